@@ -1,0 +1,211 @@
+/* cvpb200 — B200-native cone-beam projector pair (CVP exact/relaxed, Siddon-K,
+ * TT footprint) behind a plain C ABI.
+ *
+ * This is the drop-in boundary for the reference's C++ operator API
+ * (/root/reference/proj/include/cbct/{geometry,cvp,siddon,solver}.hpp). Every
+ * entry point cites the reference interface it replaces. No torch or CUDA types
+ * cross this boundary: device buffers are raw pointers, streams are opaque
+ * `void*` (a cudaStream_t; NULL = the legacy default stream).
+ *
+ * Data layout (identical to the reference so callers need no reshuffle):
+ *   volume     float32[N3][N2][N1]        (i fastest, k slowest; geometry.hpp:34-36)
+ *   projection float32[V][rows][cols]     (view-major, rows top->bottom; volume.hpp:23-46)
+ * The *_host entry points take the reference's float64 host buffers instead.
+ *
+ * Errors: every call returns a cvpb_status. The code maps 1:1 onto the
+ * exception type the reference throws for the same condition; the message is
+ * available from cvpb_last_error() (thread-local).
+ */
+#ifndef CVPB200_H
+#define CVPB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CVPB_ABI_VERSION 1
+
+typedef enum cvpb_status {
+    CVPB_OK = 0,
+    CVPB_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    CVPB_RUNTIME_ERROR = 2,    /* std::runtime_error */
+    CVPB_OUT_OF_RANGE = 3,     /* std::out_of_range */
+    CVPB_DOMAIN_ERROR = 4,     /* std::domain_error */
+    CVPB_CUDA_ERROR = 5,       /* device failure (reported as std::runtime_error) */
+    CVPB_NO_DEVICE = 6         /* no CUDA device: the path has no CPU fallback */
+} cvpb_status;
+
+/* VolumeGeometry (geometry.hpp:15-39): N1 x N2 x N3 voxels of a1 x a2 x a3 mm,
+ * box centred at the world origin. */
+typedef struct cvpb_volume_geometry {
+    int counts[3];
+    double voxel_size[3];
+} cvpb_volume_geometry;
+
+/* DetectorGeometry (geometry.hpp:43-56). */
+typedef struct cvpb_detector_geometry {
+    int rows;
+    int cols;
+    double pixel_width;  /* b1, along chi1 (columns) */
+    double pixel_height; /* b2, along chi2 (rows) */
+} cvpb_detector_geometry;
+
+/* ViewGeometry (geometry.hpp:70-123): source, frame rows (e_u, e_v, e_w),
+ * focal length f, principal point (pixels), pixel size (mm). 17 doubles. */
+typedef struct cvpb_view {
+    double source[3];
+    double frame[9];
+    double focal_length;
+    double principal_point[2];
+    double pixel_size[2];
+} cvpb_view;
+
+/* CvpOptions (cvp.hpp:13-22); enum values follow the reference's declaration
+ * order. Defaults: {CVPB_SCALING_EXACT, 1, CVPB_PRECISION_EXACT, CVPB_R_CUT_CENTROID}. */
+enum { CVPB_SCALING_COS = 0, CVPB_SCALING_EXACT = 1 };
+enum { CVPB_PRECISION_EXACT = 0 /* CvpPrecision::Double */, CVPB_PRECISION_RELAXED = 1 /* ::Single */ };
+enum { CVPB_R_VOXEL_CENTER = 0, CVPB_R_CUT_CENTROID = 1 };
+typedef struct cvpb_cvp_options {
+    int scaling;
+    int elevation_correction;
+    int precision;
+    int r_estimate;
+} cvpb_cvp_options;
+
+/* ExecPolicy (exec.hpp:6-15). threads is ignored on the device; deterministic
+ * selects a fixed-order (atomic-free) forward flush; allow_expensive gates
+ * Siddon K >= 128 exactly as the reference does (siddon.cpp:107-113). */
+typedef struct cvpb_exec_policy {
+    int threads;
+    int deterministic;
+    int allow_expensive;
+} cvpb_exec_policy;
+
+/* PixelRoi (siddon.hpp:28-33): half-open ranges, end < 0 = full extent. */
+typedef struct cvpb_pixel_roi {
+    int row_begin;
+    int row_end;
+    int col_begin;
+    int col_end;
+} cvpb_pixel_roi;
+
+/* TT footprint options (no reference symbol: SPEC.md:8 leaves TT out; the
+ * build defines it after Long, Fessler & Balter 2010, SF-TT with the A2
+ * amplitude). */
+typedef struct cvpb_tt_options {
+    int amplitude; /* 0 = A1 (ray through voxel centre), 1 = A2 (per-pixel ray) */
+} cvpb_tt_options;
+
+typedef struct cvpb_context cvpb_context;
+
+/* ---- library / context -------------------------------------------------- */
+int cvpb_abi_version(void);
+const char* cvpb_last_error(void);
+int cvpb_device_count(int* out);
+int cvpb_context_create(int device, cvpb_context** out);
+void cvpb_context_destroy(cvpb_context* ctx);
+
+/* Upload one scene. Replaces the reference's per-call view list
+ * (std::span<const ViewGeometry>, cvp.hpp:87-99) with a resident one: per-view
+ * constants (camera rows, source, 1/f ...) are precomputed in float64 on the
+ * host and kept in device memory; pixel-scale images are built once per
+ * distinct intrinsics (ScaleCache, cvp.cpp:264-302). Validates every view like
+ * check_view_consistency (cvp.cpp:237-247). */
+int cvpb_set_geometry(cvpb_context* ctx, const cvpb_volume_geometry* vol,
+                      const cvpb_detector_geometry* det, int n_views, const cvpb_view* views);
+int cvpb_get_counts(const cvpb_context* ctx, int* n_views, size_t* volume_elems,
+                    size_t* projection_elems);
+
+/* ---- geometry helpers (geometry.cpp) ------------------------------------ */
+/* ViewGeometry::make (geometry.cpp:52-88): validates and snaps the frame. */
+int cvpb_view_make(const double source[3], const double frame[9], double focal_length,
+                   const double principal_point[2], const double pixel_size[2], cvpb_view* out);
+/* make_circular_trajectory (geometry.cpp:182-210). */
+int cvpb_make_circular_trajectory(double sid, double sdd, int n_views, double arc_deg,
+                                  const cvpb_detector_geometry* det, cvpb_view* out);
+/* ViewGeometry::standard_matrix / from_standard_matrix (geometry.cpp:120-180). */
+int cvpb_view_standard_matrix(const cvpb_view* view, double P[12]);
+int cvpb_view_from_standard_matrix(const double P[12], const double pixel_size[2], cvpb_view* out);
+/* ViewGeometry::project_point (geometry.cpp:90-96). */
+int cvpb_view_project_point(const cvpb_view* view, const double x[3], double chi[2]);
+/* pixel_scale_cos / pixel_scale_exact (cvp.cpp:570-605), host float64. */
+int cvpb_pixel_scale(const cvpb_view* view, const cvpb_detector_geometry* det, int exact, int m,
+                     int n, double* out);
+/* fill_uniform01 (solver.cpp:30-33): mt19937_64, (x >> 11) * 2^-53. */
+int cvpb_fill_uniform01(double* out, size_t n, uint64_t seed);
+
+/* ---- CVP (cvp.hpp:81-99) — device buffers ------------------------------- */
+/* project_cvp_into (cvp.cpp:615-626): overwrites views [view_begin,
+ * view_begin+view_count) of d_proj (which points at view 0's image of that
+ * range, i.e. the caller's slice). */
+int cvpb_project_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts,
+                     const cvpb_exec_policy* exec, const float* d_volume, float* d_proj,
+                     int view_begin, int view_count, void* stream);
+/* backproject_cvp_into (cvp.cpp:636-650): accumulate = 0 zero-fills d_volume
+ * first (reference semantics, cvp.cpp:645); 1 adds (view-chunked / per-rank
+ * partial volumes). */
+int cvpb_backproject_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts,
+                         const cvpb_exec_policy* exec, const float* d_proj, float* d_volume,
+                         int view_begin, int view_count, int accumulate, void* stream);
+
+/* ---- CVP — reference-facing host path (float64 host buffers, H2D/D2H inside) */
+int cvpb_project_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
+                          const cvpb_exec_policy* exec, const double* volume, double* proj,
+                          double* view_seconds);
+int cvpb_backproject_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
+                              const cvpb_exec_policy* exec, const double* proj, double* volume,
+                              double* view_seconds);
+
+/* collect_cut_records (cvp.cpp:652-689) evaluated by the DEVICE kernel's own
+ * cut/row code for voxel (i,j,k) under view `view`; clamp = 0 reproduces the
+ * reference (no detector clamping). Writes at most cap records, total in *n_out. */
+int cvpb_collect_cut_records(cvpb_context* ctx, const cvpb_cvp_options* opts, int view, int i,
+                             int j, int k, int clamp, int cap, int* rows, int* cols,
+                             double* volume, double* inv_r2, int* n_out);
+/* Device pixel-scale image of one view (float64 [rows][cols]) for checking. */
+int cvpb_scale_image(cvpb_context* ctx, int view, int exact, double* out_host);
+
+/* ---- Siddon-K (siddon.hpp:34-55) ---------------------------------------- */
+int cvpb_project_siddon(cvpb_context* ctx, int k_per_edge, const cvpb_pixel_roi* roi,
+                        const cvpb_exec_policy* exec, const float* d_volume, float* d_proj,
+                        int view_begin, int view_count, void* stream);
+int cvpb_backproject_siddon(cvpb_context* ctx, int k_per_edge, const cvpb_exec_policy* exec,
+                            const float* d_proj, float* d_volume, int view_begin, int view_count,
+                            int accumulate, void* stream);
+
+/* ---- TT footprint (new; see cvpb_tt_options) ----------------------------- */
+int cvpb_project_tt(cvpb_context* ctx, const cvpb_tt_options* opts, const float* d_volume,
+                    float* d_proj, int view_begin, int view_count, void* stream);
+int cvpb_backproject_tt(cvpb_context* ctx, const cvpb_tt_options* opts, const float* d_proj,
+                        float* d_volume, int view_begin, int view_count, int accumulate,
+                        void* stream);
+
+/* ---- device vector ops for CGLS (solver.cpp:15-106) ---------------------- */
+/* Compensated float64 dot of two float32 device vectors (dot_kahan,
+ * solver.cpp:15-24); result written to *out_host after a stream sync. */
+int cvpb_vec_dot(cvpb_context* ctx, const float* a, const float* b, size_t n, double* out_host,
+                 void* stream);
+/* y += alpha * x */
+int cvpb_vec_axpy(cvpb_context* ctx, double alpha, const float* x, float* y, size_t n,
+                  void* stream);
+/* p = s + beta * p */
+int cvpb_vec_xpby(cvpb_context* ctx, const float* s, double beta, float* p, size_t n,
+                  void* stream);
+/* 1 if every element is finite (cgls check_finite, solver.cpp:60-65). */
+int cvpb_vec_all_finite(cvpb_context* ctx, const float* x, size_t n, int* out_host, void* stream);
+
+/* Device-resident CGLS (cgls, solver.cpp:55-106) over the context's scene.
+ * projector: 0 = CVP (cvp_opts), 1 = Siddon-K (k_per_edge), 2 = TT.
+ * d_b is the data (float32 stack, not modified), d_x receives the iterate;
+ * residual_norms[iterations+1] receives ||b - A x_k|| (entry 0 = ||b||).
+ * Scratch vectors are owned by the context. */
+int cvpb_cgls(cvpb_context* ctx, int projector, const cvpb_cvp_options* cvp_opts, int k_per_edge,
+              const float* d_b, float* d_x, int iterations, double* residual_norms, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CVPB200_H */

@@ -1,0 +1,985 @@
+// C-ABI of libcvpb200: contexts, scene upload, validation, dispatch to the
+// sm_100a kernels, the reference-facing float64 host path and the
+// device-resident CGLS driver. See include/cvpb200.h for the contract.
+//
+// Host geometry follows the reference's semantics (file:line cited per
+// function) so that error types, messages and view parameters match; the
+// numeric hot path lives in the .cu files.
+#include "cvpb200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <random>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+using cvpb::Scene;
+using cvpb::ViewConst;
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+
+#define CVPB_CUDA(call)                                                                    \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(CVPB_CUDA_ERROR, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                             " at " #call);                                \
+    } while (0)
+
+#define CVPB_TRY(call)                 \
+    do {                               \
+        int rc_ = (call);              \
+        if (rc_ != CVPB_OK) return rc_; \
+    } while (0)
+
+// ---- tiny float64 vector helpers ------------------------------------------
+struct D3 {
+    double x, y, z;
+};
+inline D3 d3(const double* p) { return {p[0], p[1], p[2]}; }
+inline double dot(D3 a, D3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+inline D3 cross(D3 a, D3 b) {
+    return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+inline D3 add(D3 a, D3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+inline D3 sub(D3 a, D3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+inline D3 mul(double s, D3 a) { return {s * a.x, s * a.y, s * a.z}; }
+inline double norm(D3 a) { return std::sqrt(dot(a, a)); }
+
+const double kPi = 3.14159265358979323846;
+
+// ---- view validation (ViewGeometry::make, geometry.cpp:52-88) --------------
+int view_make(const double s[3], const double fr[9], double f, const double pp[2],
+              const double b[2], cvpb_view* out) {
+    for (int i = 0; i < 3; ++i)
+        if (!std::isfinite(s[i])) return fail(CVPB_INVALID_ARGUMENT, "source is not finite");
+    if (!std::isfinite(f)) return fail(CVPB_INVALID_ARGUMENT, "focal length is not finite");
+    if (f <= 0.0) return fail(CVPB_INVALID_ARGUMENT, "focal length must be positive");
+    if (b[0] <= 0.0 || b[1] <= 0.0) return fail(CVPB_INVALID_ARGUMENT, "pixel sizes must be positive");
+    const double tol = 1e-12;
+    D3 row[3] = {d3(fr), d3(fr + 3), d3(fr + 6)};
+    for (int r = 0; r < 3; ++r)
+        for (int c = r; c < 3; ++c) {
+            const double want = r == c ? 1.0 : 0.0;
+            if (std::abs(dot(row[r], row[c]) - want) > tol)
+                return fail(CVPB_INVALID_ARGUMENT, "detector frame is not orthonormal");
+        }
+    if (std::abs(dot(row[0], cross(row[1], row[2])) - 1.0) > 1e-10)
+        return fail(CVPB_INVALID_ARGUMENT, "detector frame must be right-handed");
+    if (std::abs(row[1].x) > tol || std::abs(row[1].y) > tol || std::abs(row[1].z + 1.0) > tol)
+        return fail(CVPB_INVALID_ARGUMENT, "chi2 axis must be antiparallel to world x3");
+    cvpb_view v;
+    std::memcpy(v.source, s, sizeof v.source);
+    std::memcpy(v.frame, fr, sizeof v.frame);
+    v.frame[3] = 0.0;
+    v.frame[4] = 0.0;
+    v.frame[5] = -1.0;
+    v.focal_length = f;
+    v.principal_point[0] = pp[0];
+    v.principal_point[1] = pp[1];
+    v.pixel_size[0] = b[0];
+    v.pixel_size[1] = b[1];
+    *out = v;
+    return CVPB_OK;
+}
+
+// Camera rows C = K*Q (geometry.cpp:82-86).
+void camera(const cvpb_view& v, D3 cam[3]) {
+    const D3 eu = d3(v.frame), ev = d3(v.frame + 3), ew = d3(v.frame + 6);
+    const double fu = v.focal_length / v.pixel_size[0], fv = v.focal_length / v.pixel_size[1];
+    cam[0] = add(mul(fu, eu), mul(v.principal_point[0], ew));
+    cam[1] = add(mul(fv, ev), mul(v.principal_point[1], ew));
+    cam[2] = ew;
+}
+
+ViewConst view_const(const cvpb_view& v) {
+    ViewConst c{};
+    D3 cam[3];
+    camera(v, cam);
+    c.sx = v.source[0];
+    c.sy = v.source[1];
+    c.s3 = v.source[2];
+    c.w1x = cam[0].x;
+    c.w1y = cam[0].y;
+    c.w3x = cam[2].x;
+    c.w3y = cam[2].y;
+    c.pp1 = v.principal_point[0];
+    c.pp2 = v.principal_point[1];
+    c.f_over_b2 = v.focal_length / v.pixel_size[1];
+    c.b2_over_f = v.pixel_size[1] / v.focal_length;
+    const D3 eu = d3(v.frame), ev = d3(v.frame + 3), ew = d3(v.frame + 6), s = d3(v.source);
+    const D3 du = mul(v.pixel_size[0], eu), dv = mul(v.pixel_size[1], ev);
+    const D3 base = sub(sub(add(s, mul(v.focal_length, ew)), mul(v.principal_point[0], du)),
+                        mul(v.principal_point[1], dv));
+    const D3 vecs[6] = {base, du, dv, eu, ev, ew};
+    double* dst[6] = {c.base, c.du, c.dv, c.eu, c.ev, c.ew};
+    for (int q = 0; q < 6; ++q) {
+        dst[q][0] = vecs[q].x;
+        dst[q][1] = vecs[q].y;
+        dst[q][2] = vecs[q].z;
+    }
+    c.f = v.focal_length;
+    c.b1 = v.pixel_size[0];
+    c.b2 = v.pixel_size[1];
+    return c;
+}
+
+// spherical_quad_area (cvp.cpp:580-599): host API keeps the reference's
+// edge-normal form and its domain checks.
+int spherical_quad_area(const D3 t[4], double* out) {
+    for (int i = 0; i < 4; ++i)
+        if (std::abs(norm(t[i]) - 1.0) > 1e-12)
+            return fail(CVPB_INVALID_ARGUMENT, "spherical quad vertices must be unit vectors");
+    D3 nrm[4];
+    for (int i = 0; i < 4; ++i) {
+        nrm[i] = cross(t[i], t[(i + 1) % 4]);
+        if (dot(nrm[i], nrm[i]) < 1e-30)
+            return fail(CVPB_DOMAIN_ERROR, "degenerate spherical quad (parallel consecutive vertices)");
+        nrm[i] = mul(1.0 / norm(nrm[i]), nrm[i]);
+    }
+    double sum = 0.0;
+    for (int i = 0; i < 4; ++i)
+        sum += std::acos(std::clamp(dot(nrm[i], nrm[(i + 1) % 4]), -1.0, 1.0));
+    const double area = 2.0 * kPi - sum;
+    if (!(area > 0.0) || !(area < 4.0 * kPi))
+        return fail(CVPB_DOMAIN_ERROR, "spherical quad area outside (0, 4*pi)");
+    *out = area;
+    return CVPB_OK;
+}
+
+bool same_intrinsics(const cvpb_view& a, const cvpb_view& b) {
+    return a.focal_length == b.focal_length && a.principal_point[0] == b.principal_point[0] &&
+           a.principal_point[1] == b.principal_point[1] && a.pixel_size[0] == b.pixel_size[0] &&
+           a.pixel_size[1] == b.pixel_size[1];
+}
+
+template <class T> struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaError_t reserve(size_t want) {
+        if (want <= n && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        cudaError_t e = cudaMalloc(&p, sizeof(T) * std::max<size_t>(want, 1));
+        if (e == cudaSuccess) n = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+}  // namespace
+
+struct cvpb_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;  // host-path / CGLS stream
+    bool has_geometry = false;
+    cvpb_volume_geometry vol{};
+    cvpb_detector_geometry det{};
+    Scene sc{};
+    std::vector<cvpb_view> views;
+    std::vector<ViewConst> vconst;
+    bool source_inside = false;     // check_view_consistency (cvp.cpp:242-246)
+    bool pixel_mismatch = false;    // (cvp.cpp:239-241)
+    bool base_reaches_source = false;  // (cvp.cpp:82-84), resolved for the whole box
+    int n_slots = 0;
+    DevBuf<ViewConst> d_views;
+    DevBuf<float> d_scale_cos, d_scale_exact;
+    DevBuf<int> d_err, d_box, d_flag;
+    DevBuf<double> d_partials, d_stage;
+    DevBuf<float> h_vol, h_proj;  // device buffers of the host path
+    DevBuf<float> cg_r, cg_q, cg_s, cg_p;
+    DevBuf<int> d_rec_i;
+    DevBuf<double> d_rec_d;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    size_t nvox() const { return size_t(vol.counts[0]) * vol.counts[1] * vol.counts[2]; }
+    size_t npx_view() const { return size_t(det.rows) * det.cols; }
+};
+
+namespace {
+
+int check_ctx(cvpb_context* ctx, bool need_geometry = true) {
+    if (!ctx) return fail(CVPB_INVALID_ARGUMENT, "null context");
+    if (need_geometry && !ctx->has_geometry)
+        return fail(CVPB_INVALID_ARGUMENT, "no geometry set on the context");
+    if (cudaSetDevice(ctx->device) != cudaSuccess)
+        return fail(CVPB_CUDA_ERROR, "cannot select the context's device");
+    return CVPB_OK;
+}
+
+int check_range(cvpb_context* ctx, int view_begin, int view_count) {
+    if (view_begin < 0 || view_count < 0 || view_begin + view_count > int(ctx->views.size()))
+        return fail(CVPB_INVALID_ARGUMENT, "projection stack does not match views");
+    return CVPB_OK;
+}
+
+// check_view_consistency semantics (cvp.cpp:237-247), evaluated per call like
+// the reference so the error surfaces from project/backproject.
+int check_scene_views(cvpb_context* ctx) {
+    if (ctx->pixel_mismatch)
+        return fail(CVPB_INVALID_ARGUMENT, "view pixel size does not match the detector geometry");
+    if (ctx->source_inside)
+        return fail(CVPB_RUNTIME_ERROR, "unsupported configuration: source inside the volume box");
+    return CVPB_OK;
+}
+
+int check_cvp_options(const cvpb_cvp_options* o) {
+    if (!o) return fail(CVPB_INVALID_ARGUMENT, "null CVP options");
+    if ((o->scaling != 0 && o->scaling != 1) || (o->precision != 0 && o->precision != 1) ||
+        (o->r_estimate != 0 && o->r_estimate != 1))
+        return fail(CVPB_INVALID_ARGUMENT, "invalid CVP options");
+    return CVPB_OK;
+}
+
+int check_siddon_k(int k, const cvpb_exec_policy* exec) {
+    if (k < 1) return fail(CVPB_INVALID_ARGUMENT, "Siddon K must be at least 1");
+    if (k >= 128 && !(exec && exec->allow_expensive))
+        return fail(CVPB_INVALID_ARGUMENT,
+                    "Siddon-K with K >= 128 is a deliberately expensive ground-truth "
+                    "configuration; set ExecPolicy::allow_expensive to confirm");
+    return CVPB_OK;
+}
+
+int device_error(cvpb_context* ctx, cudaStream_t st) {
+    int h = 0;
+    CVPB_CUDA(cudaMemcpyAsync(&h, ctx->d_err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CVPB_CUDA(cudaStreamSynchronize(st));
+    if (h == 0) return CVPB_OK;
+    int zero = 0;
+    CVPB_CUDA(cudaMemcpyAsync(ctx->d_err.p, &zero, sizeof(int), cudaMemcpyHostToDevice, st));
+    CVPB_CUDA(cudaStreamSynchronize(st));
+    if (h & cvpb::kDevSourcePlane)
+        return fail(CVPB_RUNTIME_ERROR, "numerical degeneracy: voxel base reaches the source plane");
+    return fail(CVPB_DOMAIN_ERROR, "centroid of a degenerate polygon");
+}
+
+int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_policy* exec,
+            bool forward, const float* vol_in, float* vol_out, const float* proj_in,
+            float* proj_out, int view_begin, int view_count, int accumulate, cudaStream_t st) {
+    CVPB_TRY(check_ctx(ctx));
+    CVPB_TRY(check_cvp_options(opts));
+    CVPB_TRY(check_range(ctx, view_begin, view_count));
+    CVPB_TRY(check_scene_views(ctx));
+    if (ctx->base_reaches_source)
+        return fail(CVPB_RUNTIME_ERROR, "numerical degeneracy: voxel base reaches the source plane");
+    cvpb::CvpLaunch L{};
+    L.sc = ctx->sc;
+    L.views = ctx->d_views.p;
+    L.scales = opts->scaling == CVPB_SCALING_EXACT ? ctx->d_scale_exact.p : ctx->d_scale_cos.p;
+    L.vol_in = vol_in;
+    L.vol_out = vol_out;
+    L.proj_in = proj_in;
+    L.proj_out = proj_out;
+    L.view_begin = view_begin;
+    L.view_count = view_count;
+    L.forward = forward ? 1 : 0;
+    L.exact = opts->precision == CVPB_PRECISION_EXACT ? 1 : 0;
+    L.elevation_correction = opts->elevation_correction ? 1 : 0;
+    L.cut_centroid = opts->r_estimate == CVPB_R_CUT_CENTROID ? 1 : 0;
+    L.accumulate = accumulate;
+    L.deterministic = exec ? exec->deterministic : 0;
+    L.err = ctx->d_err.p;
+    if (!forward && view_count == 0 && !accumulate) {
+        CVPB_CUDA(cudaMemsetAsync(vol_out, 0, sizeof(float) * ctx->nvox(), st));
+        return CVPB_OK;
+    }
+    CVPB_CUDA(cvpb::launch_cvp(L, st));
+    return CVPB_OK;
+}
+
+int upload_scales(cvpb_context* ctx) {
+    // distinct intrinsics -> one scale image per slot (ScaleCache, cvp.cpp:264-302)
+    std::vector<int> slot_view;
+    for (size_t v = 0; v < ctx->views.size(); ++v) {
+        int slot = -1;
+        for (size_t s = 0; s < slot_view.size(); ++s)
+            if (same_intrinsics(ctx->views[slot_view[s]], ctx->views[v])) {
+                slot = int(s);
+                break;
+            }
+        if (slot < 0) {
+            slot = int(slot_view.size());
+            slot_view.push_back(int(v));
+        }
+        ctx->vconst[v].scale_slot = slot;
+    }
+    ctx->n_slots = int(slot_view.size());
+    const size_t npx = ctx->npx_view();
+    CVPB_CUDA(ctx->d_scale_cos.reserve(npx * ctx->n_slots));
+    CVPB_CUDA(ctx->d_scale_exact.reserve(npx * ctx->n_slots));
+    for (int s = 0; s < ctx->n_slots; ++s) {
+        const cvpb_view& v = ctx->views[slot_view[s]];
+        for (int exact = 0; exact < 2; ++exact) {
+            float* dst = (exact ? ctx->d_scale_exact.p : ctx->d_scale_cos.p) + npx * s;
+            CVPB_CUDA(cvpb::launch_scale_image(v.focal_length, v.principal_point[0],
+                                               v.principal_point[1], v.pixel_size[0],
+                                               v.pixel_size[1], ctx->det.rows, ctx->det.cols,
+                                               exact, dst, nullptr, ctx->stream));
+        }
+    }
+    return CVPB_OK;
+}
+
+int ensure_host_buffers(cvpb_context* ctx) {
+    const size_t nv = ctx->nvox(), np = ctx->npx_view() * ctx->views.size();
+    CVPB_CUDA(ctx->h_vol.reserve(nv));
+    CVPB_CUDA(ctx->h_proj.reserve(np));
+    CVPB_CUDA(ctx->d_stage.reserve(std::max(nv, np)));
+    return CVPB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cvpb_abi_version(void) { return CVPB_ABI_VERSION; }
+
+const char* cvpb_last_error(void) { return g_error.c_str(); }
+
+int cvpb_device_count(int* out) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) n = 0;
+    if (out) *out = n;
+    return CVPB_OK;
+}
+
+int cvpb_context_create(int device, cvpb_context** out) {
+    if (!out) return fail(CVPB_INVALID_ARGUMENT, "null output pointer");
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        return fail(CVPB_NO_DEVICE, "no CUDA device available (cvpb200 has no CPU fallback)");
+    if (device < 0 || device >= n) return fail(CVPB_INVALID_ARGUMENT, "device index out of range");
+    CVPB_CUDA(cudaSetDevice(device));
+    auto* ctx = new cvpb_context();
+    ctx->device = device;
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        ctx->d_err.reserve(1) != cudaSuccess || ctx->d_box.reserve(6) != cudaSuccess ||
+        ctx->d_flag.reserve(1) != cudaSuccess ||
+        ctx->d_partials.reserve(cvpb::dot_partials_count()) != cudaSuccess ||
+        cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
+        cvpb_context_destroy(ctx);
+        return fail(CVPB_CUDA_ERROR, "context allocation failed");
+    }
+    cudaMemset(ctx->d_err.p, 0, sizeof(int));
+    *out = ctx;
+    return CVPB_OK;
+}
+
+void cvpb_context_destroy(cvpb_context* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto* b : {&ctx->d_scale_cos, &ctx->d_scale_exact, &ctx->h_vol, &ctx->h_proj, &ctx->cg_r,
+                    &ctx->cg_q, &ctx->cg_s, &ctx->cg_p})
+        b->release();
+    ctx->d_views.release();
+    ctx->d_err.release();
+    ctx->d_box.release();
+    ctx->d_flag.release();
+    ctx->d_partials.release();
+    ctx->d_stage.release();
+    ctx->d_rec_i.release();
+    ctx->d_rec_d.release();
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int cvpb_set_geometry(cvpb_context* ctx, const cvpb_volume_geometry* vol,
+                      const cvpb_detector_geometry* det, int n_views, const cvpb_view* views) {
+    CVPB_TRY(check_ctx(ctx, false));
+    if (!vol || !det || (n_views > 0 && !views)) return fail(CVPB_INVALID_ARGUMENT, "null geometry");
+    // VolumeGeometry::make / DetectorGeometry::make (geometry.cpp:23-50)
+    for (int c : vol->counts)
+        if (c <= 0) return fail(CVPB_INVALID_ARGUMENT, "voxel counts must be positive");
+    for (double a : vol->voxel_size) {
+        if (!std::isfinite(a)) return fail(CVPB_INVALID_ARGUMENT, "voxel size is not finite");
+        if (a <= 0.0) return fail(CVPB_INVALID_ARGUMENT, "voxel sizes must be positive");
+    }
+    if (det->rows <= 0 || det->cols <= 0)
+        return fail(CVPB_INVALID_ARGUMENT, "detector counts must be positive");
+    for (double b : {det->pixel_width, det->pixel_height}) {
+        if (!std::isfinite(b)) return fail(CVPB_INVALID_ARGUMENT, "pixel size is not finite");
+        if (b <= 0.0) return fail(CVPB_INVALID_ARGUMENT, "pixel sizes must be positive");
+    }
+    if (n_views < 0) return fail(CVPB_INVALID_ARGUMENT, "negative view count");
+    ctx->has_geometry = false;
+    ctx->vol = *vol;
+    ctx->det = *det;
+    ctx->views.assign(views, views + n_views);
+    for (auto& v : ctx->views) {  // re-validate and snap like ViewGeometry::make
+        cvpb_view snapped;
+        CVPB_TRY(view_make(v.source, v.frame, v.focal_length, v.principal_point, v.pixel_size,
+                           &snapped));
+        v = snapped;
+    }
+    Scene& sc = ctx->sc;
+    sc.n1 = vol->counts[0];
+    sc.n2 = vol->counts[1];
+    sc.n3 = vol->counts[2];
+    sc.a1 = vol->voxel_size[0];
+    sc.a2 = vol->voxel_size[1];
+    sc.a3 = vol->voxel_size[2];
+    // min_corner = extent * -0.5 (geometry.hpp:28-29)
+    sc.minx = (sc.n1 * sc.a1) * -0.5;
+    sc.miny = (sc.n2 * sc.a2) * -0.5;
+    sc.minz = (sc.n3 * sc.a3) * -0.5;
+    sc.rows = det->rows;
+    sc.cols = det->cols;
+    sc.pw = det->pixel_width;
+    sc.ph = det->pixel_height;
+    ctx->vconst.resize(n_views);
+    ctx->source_inside = ctx->pixel_mismatch = ctx->base_reaches_source = false;
+    const double lo[3] = {sc.minx, sc.miny, sc.minz};
+    const double hi[3] = {sc.minx + sc.n1 * sc.a1, sc.miny + sc.n2 * sc.a2, sc.minz + sc.n3 * sc.a3};
+    for (int v = 0; v < n_views; ++v) {
+        const cvpb_view& vw = ctx->views[v];
+        ctx->vconst[v] = view_const(vw);
+        if (std::abs(vw.pixel_size[0] - det->pixel_width) > 1e-9 ||
+            std::abs(vw.pixel_size[1] - det->pixel_height) > 1e-9)
+            ctx->pixel_mismatch = true;
+        const double* s = vw.source;
+        if (s[0] > lo[0] && s[0] < hi[0] && s[1] > lo[1] && s[1] < hi[1] && s[2] > lo[2] &&
+            s[2] < hi[2])
+            ctx->source_inside = true;
+        // every voxel-base corner is a convex combination of the box's base
+        // corners and depth is affine, so checking the 4 box corners decides
+        // the reference's per-voxel depth test (cvp.cpp:82-84) for all voxels
+        const ViewConst& c = ctx->vconst[v];
+        for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b) {
+                const double px = (a ? hi[0] : lo[0]) - c.sx, py = (b ? hi[1] : lo[1]) - c.sy;
+                if (!(c.w3x * px + c.w3y * py > 0.0)) ctx->base_reaches_source = true;
+            }
+    }
+    CVPB_CUDA(ctx->d_views.reserve(std::max(n_views, 1)));
+    if (n_views > 0)
+        CVPB_CUDA(cudaMemcpyAsync(ctx->d_views.p, ctx->vconst.data(), sizeof(ViewConst) * n_views,
+                                  cudaMemcpyHostToDevice, ctx->stream));
+    CVPB_TRY(upload_scales(ctx));
+    if (n_views > 0)  // scale slots were assigned after the first copy
+        CVPB_CUDA(cudaMemcpyAsync(ctx->d_views.p, ctx->vconst.data(), sizeof(ViewConst) * n_views,
+                                  cudaMemcpyHostToDevice, ctx->stream));
+    CVPB_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->has_geometry = true;
+    return CVPB_OK;
+}
+
+int cvpb_get_counts(const cvpb_context* ctx, int* n_views, size_t* volume_elems,
+                    size_t* projection_elems) {
+    if (!ctx || !ctx->has_geometry) return fail(CVPB_INVALID_ARGUMENT, "no geometry set on the context");
+    if (n_views) *n_views = int(ctx->views.size());
+    if (volume_elems) *volume_elems = ctx->nvox();
+    if (projection_elems) *projection_elems = ctx->npx_view() * ctx->views.size();
+    return CVPB_OK;
+}
+
+// ---- geometry helpers ------------------------------------------------------
+
+int cvpb_view_make(const double source[3], const double frame[9], double focal_length,
+                   const double principal_point[2], const double pixel_size[2], cvpb_view* out) {
+    if (!source || !frame || !principal_point || !pixel_size || !out)
+        return fail(CVPB_INVALID_ARGUMENT, "null argument");
+    return view_make(source, frame, focal_length, principal_point, pixel_size, out);
+}
+
+// make_circular_trajectory (geometry.cpp:182-210): source on +x1 at w = 0,
+// counter-clockwise; 360 deg arcs are open circles, shorter arcs inclusive.
+int cvpb_make_circular_trajectory(double sid, double sdd, int n_views, double arc_deg,
+                                  const cvpb_detector_geometry* det, cvpb_view* out) {
+    if (!det || !out) return fail(CVPB_INVALID_ARGUMENT, "null argument");
+    if (n_views <= 0) return fail(CVPB_INVALID_ARGUMENT, "need at least one view");
+    if (!(sid > 0.0) || !(sdd > 0.0)) return fail(CVPB_INVALID_ARGUMENT, "distances must be positive");
+    if (!(arc_deg > 0.0) || arc_deg > 360.0)
+        return fail(CVPB_INVALID_ARGUMENT, "arc must lie in (0, 360] degrees");
+    const double step = std::abs(arc_deg - 360.0) < 1e-9 ? 360.0 / n_views
+                                                         : (n_views > 1 ? arc_deg / (n_views - 1) : 0.0);
+    const double pp[2] = {(det->cols - 1) * 0.5, (det->rows - 1) * 0.5};
+    const double b[2] = {det->pixel_width, det->pixel_height};
+    for (int v = 0; v < n_views; ++v) {
+        const double w = v * step * kPi / 180.0;
+        const double c = std::cos(w), s = std::sin(w);
+        const double src[3] = {sid * c, sid * s, 0.0};
+        const D3 ew{-c, -s, 0.0}, ev{0.0, 0.0, -1.0};
+        const D3 eu = cross(ev, ew);
+        const double fr[9] = {eu.x, eu.y, eu.z, ev.x, ev.y, ev.z, ew.x, ew.y, ew.z};
+        CVPB_TRY(view_make(src, fr, sdd, pp, b, &out[v]));
+    }
+    return CVPB_OK;
+}
+
+// standard_matrix [C | -C s] (geometry.cpp:120-131).
+int cvpb_view_standard_matrix(const cvpb_view* view, double P[12]) {
+    if (!view || !P) return fail(CVPB_INVALID_ARGUMENT, "null argument");
+    D3 cam[3];
+    camera(*view, cam);
+    const D3 s = d3(view->source);
+    for (int r = 0; r < 3; ++r) {
+        P[4 * r + 0] = cam[r].x;
+        P[4 * r + 1] = cam[r].y;
+        P[4 * r + 2] = cam[r].z;
+        P[4 * r + 3] = -dot(cam[r], s);
+    }
+    return CVPB_OK;
+}
+
+// from_standard_matrix (geometry.cpp:133-180): factor P = [B | p4] of any
+// scale into source, frame, focal length and principal point.
+int cvpb_view_from_standard_matrix(const double P[12], const double pixel_size[2], cvpb_view* out) {
+    if (!P || !pixel_size || !out) return fail(CVPB_INVALID_ARGUMENT, "null argument");
+    for (int i = 0; i < 12; ++i)
+        if (!std::isfinite(P[i])) return fail(CVPB_INVALID_ARGUMENT, "matrix entry is not finite");
+    const D3 B0{P[0], P[1], P[2]}, B1{P[4], P[5], P[6]}, B2{P[8], P[9], P[10]};
+    const D3 p4{P[3], P[7], P[11]};
+    const double detB = dot(B0, cross(B1, B2));
+    if (std::abs(detB) < 1e-300) return fail(CVPB_DOMAIN_ERROR, "matrix is singular");
+    // B^-1 columns are cross products of row pairs / det
+    const D3 c0 = mul(1.0 / detB, cross(B1, B2)), c1 = mul(1.0 / detB, cross(B2, B0)),
+             c2 = mul(1.0 / detB, cross(B0, B1));
+    const D3 binv_p4{c0.x * p4.x + c1.x * p4.y + c2.x * p4.z, c0.y * p4.x + c1.y * p4.y + c2.y * p4.z,
+                     c0.z * p4.x + c1.z * p4.y + c2.z * p4.z};
+    const D3 src = mul(-1.0, binv_p4);
+    double scl = norm(B2);
+    if (!(scl > 0.0)) return fail(CVPB_INVALID_ARGUMENT, "degenerate projection matrix");
+    if (detB < 0.0) scl = -scl;
+    const D3 C0 = mul(1.0 / scl, B0), C1 = mul(1.0 / scl, B1), C2 = mul(1.0 / scl, B2);
+    D3 ew = C2;
+    const double pp2 = dot(C1, ew);
+    const D3 ev_f = sub(C1, mul(pp2, ew));
+    const double fv = norm(ev_f);
+    const double pp1 = dot(C0, ew);
+    const D3 eu_f = sub(C0, mul(pp1, ew));
+    const double fu = norm(eu_f);
+    if (!(fu > 0.0) || !(fv > 0.0)) return fail(CVPB_INVALID_ARGUMENT, "degenerate projection matrix");
+    const double f = fv * pixel_size[1];
+    if (std::abs(fu * pixel_size[0] - f) > 1e-6 * std::abs(f))
+        return fail(CVPB_INVALID_ARGUMENT,
+                    "projection matrix focal lengths are inconsistent with the pixel sizes");
+    const D3 ev = mul(1.0 / fv, ev_f);
+    if (std::abs(ev.x) > 1e-6 || std::abs(ev.y) > 1e-6 || std::abs(ev.z + 1.0) > 1e-6)
+        return fail(CVPB_INVALID_ARGUMENT, "projection matrix violates the detector row convention");
+    const D3 evs{0.0, 0.0, -1.0};
+    ew.z = 0.0;
+    const double ewn = norm(ew);
+    if (!(ewn > 0.0)) return fail(CVPB_DOMAIN_ERROR, "cannot normalize zero vector");
+    ew = mul(1.0 / ewn, ew);
+    const D3 eu = cross(evs, ew);
+    const double s[3] = {src.x, src.y, src.z};
+    const double fr[9] = {eu.x, eu.y, eu.z, evs.x, evs.y, evs.z, ew.x, ew.y, ew.z};
+    const double pp[2] = {pp1, pp2};
+    return view_make(s, fr, f, pp, pixel_size, out);
+}
+
+int cvpb_view_project_point(const cvpb_view* view, const double x[3], double chi[2]) {
+    if (!view || !x || !chi) return fail(CVPB_INVALID_ARGUMENT, "null argument");
+    D3 cam[3];
+    camera(*view, cam);
+    const D3 d = sub(d3(x), d3(view->source));
+    const double w = dot(d3(view->frame + 6), d);
+    if (!(w > 0.0))
+        return fail(CVPB_DOMAIN_ERROR, "point does not lie strictly on the detector side of the source");
+    chi[0] = dot(cam[0], d) / w;
+    chi[1] = dot(cam[1], d) / w;
+    return CVPB_OK;
+}
+
+// pixel_scale_cos / pixel_scale_exact (cvp.cpp:570-605).
+int cvpb_pixel_scale(const cvpb_view* view, const cvpb_detector_geometry* det, int exact, int m,
+                     int n, double* out) {
+    if (!view || !det || !out) return fail(CVPB_INVALID_ARGUMENT, "null argument");
+    if (m < 0 || n < 0 || m >= det->rows || n >= det->cols)
+        return fail(CVPB_OUT_OF_RANGE, "pixel outside the detector");
+    const double f = view->focal_length, pp1 = view->principal_point[0],
+                 pp2 = view->principal_point[1], b1 = view->pixel_size[0],
+                 b2 = view->pixel_size[1];
+    if (!exact) {
+        const double u = (n - pp1) * b1, v = (m - pp2) * b2;
+        const double c = f / std::sqrt(u * u + v * v + f * f);
+        *out = f * f / (det->pixel_width * det->pixel_height * c * c * c);
+        return CVPB_OK;
+    }
+    const double u0 = (n - 0.5 - pp1) * b1, u1 = (n + 0.5 - pp1) * b1;
+    const double v0 = (m - 0.5 - pp2) * b2, v1 = (m + 0.5 - pp2) * b2;
+    D3 t[4] = {{u0, v0, f}, {u1, v0, f}, {u1, v1, f}, {u0, v1, f}};
+    for (auto& q : t) q = mul(1.0 / norm(q), q);
+    double omega;
+    CVPB_TRY(spherical_quad_area(t, &omega));
+    *out = 1.0 / omega;
+    return CVPB_OK;
+}
+
+int cvpb_fill_uniform01(double* out, size_t n, uint64_t seed) {
+    if (!out && n) return fail(CVPB_INVALID_ARGUMENT, "null output");
+    std::mt19937_64 rng(seed);
+    for (size_t i = 0; i < n; ++i) out[i] = double(rng() >> 11) * 0x1.0p-53;
+    return CVPB_OK;
+}
+
+// ---- CVP --------------------------------------------------------------------
+
+int cvpb_project_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_policy* exec,
+                     const float* d_volume, float* d_proj, int view_begin, int view_count,
+                     void* stream) {
+    return run_cvp(ctx, opts, exec, true, d_volume, nullptr, nullptr, d_proj, view_begin,
+                   view_count, 0, static_cast<cudaStream_t>(stream));
+}
+
+int cvpb_backproject_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts,
+                         const cvpb_exec_policy* exec, const float* d_proj, float* d_volume,
+                         int view_begin, int view_count, int accumulate, void* stream) {
+    return run_cvp(ctx, opts, exec, false, nullptr, d_volume, d_proj, nullptr, view_begin,
+                   view_count, accumulate, static_cast<cudaStream_t>(stream));
+}
+
+int cvpb_project_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
+                          const cvpb_exec_policy* exec, const double* volume, double* proj,
+                          double* view_seconds) {
+    CVPB_TRY(check_ctx(ctx));
+    if (!volume || !proj) return fail(CVPB_INVALID_ARGUMENT, "null host buffer");
+    CVPB_TRY(ensure_host_buffers(ctx));
+    cudaStream_t st = ctx->stream;
+    const size_t nv = ctx->nvox(), np = ctx->npx_view() * ctx->views.size();
+    const int nviews = int(ctx->views.size());
+    CVPB_CUDA(cudaEventRecord(ctx->ev0, st));
+    CVPB_CUDA(cudaMemcpyAsync(ctx->d_stage.p, volume, sizeof(double) * nv, cudaMemcpyHostToDevice, st));
+    CVPB_CUDA(cvpb::launch_f64_to_f32(ctx->d_stage.p, ctx->h_vol.p, nv, st));
+    CVPB_TRY(run_cvp(ctx, opts, exec, true, ctx->h_vol.p, nullptr, nullptr, ctx->h_proj.p, 0,
+                     nviews, 0, st));
+    CVPB_CUDA(cvpb::launch_f32_to_f64(ctx->h_proj.p, ctx->d_stage.p, np, st));
+    CVPB_CUDA(cudaMemcpyAsync(proj, ctx->d_stage.p, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+    CVPB_CUDA(cudaEventRecord(ctx->ev1, st));
+    CVPB_TRY(device_error(ctx, st));
+    if (view_seconds) {
+        float ms = 0.f;
+        CVPB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        for (int v = 0; v < nviews; ++v) view_seconds[v] = ms * 1e-3 / std::max(nviews, 1);
+    }
+    return CVPB_OK;
+}
+
+int cvpb_backproject_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
+                              const cvpb_exec_policy* exec, const double* proj, double* volume,
+                              double* view_seconds) {
+    CVPB_TRY(check_ctx(ctx));
+    if (!volume || !proj) return fail(CVPB_INVALID_ARGUMENT, "null host buffer");
+    CVPB_TRY(ensure_host_buffers(ctx));
+    cudaStream_t st = ctx->stream;
+    const size_t nv = ctx->nvox(), np = ctx->npx_view() * ctx->views.size();
+    const int nviews = int(ctx->views.size());
+    CVPB_CUDA(cudaEventRecord(ctx->ev0, st));
+    CVPB_CUDA(cudaMemcpyAsync(ctx->d_stage.p, proj, sizeof(double) * np, cudaMemcpyHostToDevice, st));
+    CVPB_CUDA(cvpb::launch_f64_to_f32(ctx->d_stage.p, ctx->h_proj.p, np, st));
+    CVPB_TRY(run_cvp(ctx, opts, exec, false, nullptr, ctx->h_vol.p, ctx->h_proj.p, nullptr, 0,
+                     nviews, 0, st));
+    CVPB_CUDA(cvpb::launch_f32_to_f64(ctx->h_vol.p, ctx->d_stage.p, nv, st));
+    CVPB_CUDA(cudaMemcpyAsync(volume, ctx->d_stage.p, sizeof(double) * nv, cudaMemcpyDeviceToHost, st));
+    CVPB_CUDA(cudaEventRecord(ctx->ev1, st));
+    CVPB_TRY(device_error(ctx, st));
+    if (view_seconds) {
+        float ms = 0.f;
+        CVPB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        for (int v = 0; v < nviews; ++v) view_seconds[v] = ms * 1e-3 / std::max(nviews, 1);
+    }
+    return CVPB_OK;
+}
+
+int cvpb_collect_cut_records(cvpb_context* ctx, const cvpb_cvp_options* opts, int view, int i,
+                             int j, int k, int clamp, int cap, int* rows, int* cols,
+                             double* volume, double* inv_r2, int* n_out) {
+    CVPB_TRY(check_ctx(ctx));
+    CVPB_TRY(check_cvp_options(opts));
+    if (view < 0 || view >= int(ctx->views.size()))
+        return fail(CVPB_OUT_OF_RANGE, "view index outside the scene");
+    if (i < 0 || j < 0 || k < 0 || i >= ctx->sc.n1 || j >= ctx->sc.n2 || k >= ctx->sc.n3)
+        return fail(CVPB_OUT_OF_RANGE, "voxel index outside lattice");
+    CVPB_TRY(check_scene_views(ctx));
+    if (cap < 0) cap = 0;
+    cudaStream_t st = ctx->stream;
+    CVPB_CUDA(ctx->d_rec_i.reserve(2 * size_t(cap) + 1));
+    CVPB_CUDA(ctx->d_rec_d.reserve(2 * size_t(cap) + 1));
+    int* d_rows = ctx->d_rec_i.p;
+    int* d_cols = d_rows + cap;
+    int* d_n = d_cols + cap;
+    double* d_vol = ctx->d_rec_d.p;
+    double* d_inv = d_vol + cap;
+    CVPB_CUDA(cvpb::launch_cut_records(ctx->sc, ctx->d_views.p, view, i, j, k,
+                                       opts->precision == CVPB_PRECISION_EXACT,
+                                       opts->elevation_correction,
+                                       opts->r_estimate == CVPB_R_CUT_CENTROID, clamp, cap, d_rows,
+                                       d_cols, d_vol, d_inv, d_n, ctx->d_err.p, st));
+    int n = 0;
+    CVPB_CUDA(cudaMemcpyAsync(&n, d_n, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CVPB_TRY(device_error(ctx, st));
+    const int c = std::min(n, cap);
+    if (c > 0) {
+        if (rows) CVPB_CUDA(cudaMemcpy(rows, d_rows, sizeof(int) * c, cudaMemcpyDeviceToHost));
+        if (cols) CVPB_CUDA(cudaMemcpy(cols, d_cols, sizeof(int) * c, cudaMemcpyDeviceToHost));
+        if (volume) CVPB_CUDA(cudaMemcpy(volume, d_vol, sizeof(double) * c, cudaMemcpyDeviceToHost));
+        if (inv_r2) CVPB_CUDA(cudaMemcpy(inv_r2, d_inv, sizeof(double) * c, cudaMemcpyDeviceToHost));
+    }
+    if (n_out) *n_out = n;
+    return CVPB_OK;
+}
+
+int cvpb_scale_image(cvpb_context* ctx, int view, int exact, double* out_host) {
+    CVPB_TRY(check_ctx(ctx));
+    if (view < 0 || view >= int(ctx->views.size()))
+        return fail(CVPB_OUT_OF_RANGE, "view index outside the scene");
+    if (!out_host) return fail(CVPB_INVALID_ARGUMENT, "null output");
+    const size_t npx = ctx->npx_view();
+    DevBuf<double> tmp;
+    CVPB_CUDA(tmp.reserve(npx));
+    const cvpb_view& v = ctx->views[view];
+    cudaError_t e = cvpb::launch_scale_image(v.focal_length, v.principal_point[0],
+                                             v.principal_point[1], v.pixel_size[0], v.pixel_size[1],
+                                             ctx->det.rows, ctx->det.cols, exact, nullptr, tmp.p,
+                                             ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpy(out_host, tmp.p, sizeof(double) * npx, cudaMemcpyDeviceToHost);
+    tmp.release();
+    CVPB_CUDA(e);
+    return CVPB_OK;
+}
+
+// ---- Siddon-K -----------------------------------------------------------------
+
+int cvpb_project_siddon(cvpb_context* ctx, int k_per_edge, const cvpb_pixel_roi* roi,
+                        const cvpb_exec_policy* exec, const float* d_volume, float* d_proj,
+                        int view_begin, int view_count, void* stream) {
+    CVPB_TRY(check_ctx(ctx));
+    CVPB_TRY(check_siddon_k(k_per_edge, exec));
+    CVPB_TRY(check_range(ctx, view_begin, view_count));
+    CVPB_TRY(check_scene_views(ctx));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cvpb::SiddonLaunch L{};
+    L.sc = ctx->sc;
+    L.views = ctx->d_views.p;
+    L.vol_in = d_volume;
+    L.proj_out = d_proj;
+    L.view_begin = view_begin;
+    L.view_count = view_count;
+    L.k_per_edge = k_per_edge;
+    // resolve (siddon.cpp:125-132)
+    const int R = ctx->sc.rows, Cc = ctx->sc.cols;
+    cvpb_pixel_roi r = roi ? *roi : cvpb_pixel_roi{0, -1, 0, -1};
+    L.r0 = std::clamp(r.row_begin, 0, R);
+    L.r1 = r.row_end < 0 ? R : std::clamp(r.row_end, L.r0, R);
+    L.c0 = std::clamp(r.col_begin, 0, Cc);
+    L.c1 = r.col_end < 0 ? Cc : std::clamp(r.col_end, L.c0, Cc);
+    CVPB_CUDA(cvpb::launch_nonzero_box(d_volume, ctx->sc, ctx->d_box.p, st));
+    L.d_box = ctx->d_box.p;
+    CVPB_CUDA(cvpb::launch_siddon(L, true, st));
+    return CVPB_OK;
+}
+
+int cvpb_backproject_siddon(cvpb_context* ctx, int k_per_edge, const cvpb_exec_policy* exec,
+                            const float* d_proj, float* d_volume, int view_begin, int view_count,
+                            int accumulate, void* stream) {
+    CVPB_TRY(check_ctx(ctx));
+    CVPB_TRY(check_siddon_k(k_per_edge, exec));
+    CVPB_TRY(check_range(ctx, view_begin, view_count));
+    CVPB_TRY(check_scene_views(ctx));
+    cvpb::SiddonLaunch L{};
+    L.sc = ctx->sc;
+    L.views = ctx->d_views.p;
+    L.proj_in = d_proj;
+    L.vol_out = d_volume;
+    L.view_begin = view_begin;
+    L.view_count = view_count;
+    L.k_per_edge = k_per_edge;
+    L.accumulate = accumulate;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (view_count == 0 && !accumulate) {
+        CVPB_CUDA(cudaMemsetAsync(d_volume, 0, sizeof(float) * ctx->nvox(), st));
+        return CVPB_OK;
+    }
+    CVPB_CUDA(cvpb::launch_siddon(L, false, st));
+    return CVPB_OK;
+}
+
+// ---- TT -------------------------------------------------------------------------
+
+int cvpb_project_tt(cvpb_context* ctx, const cvpb_tt_options* opts, const float* d_volume,
+                    float* d_proj, int view_begin, int view_count, void* stream) {
+    CVPB_TRY(check_ctx(ctx));
+    CVPB_TRY(check_range(ctx, view_begin, view_count));
+    CVPB_TRY(check_scene_views(ctx));
+    cvpb::TTLaunch L{};
+    L.sc = ctx->sc;
+    L.views = ctx->d_views.p;
+    L.vol_in = d_volume;
+    L.proj_out = d_proj;
+    L.view_begin = view_begin;
+    L.view_count = view_count;
+    L.amplitude = opts ? opts->amplitude : 1;
+    CVPB_CUDA(cvpb::launch_tt(L, true, static_cast<cudaStream_t>(stream)));
+    return CVPB_OK;
+}
+
+int cvpb_backproject_tt(cvpb_context* ctx, const cvpb_tt_options* opts, const float* d_proj,
+                        float* d_volume, int view_begin, int view_count, int accumulate,
+                        void* stream) {
+    CVPB_TRY(check_ctx(ctx));
+    CVPB_TRY(check_range(ctx, view_begin, view_count));
+    CVPB_TRY(check_scene_views(ctx));
+    cvpb::TTLaunch L{};
+    L.sc = ctx->sc;
+    L.views = ctx->d_views.p;
+    L.proj_in = d_proj;
+    L.vol_out = d_volume;
+    L.view_begin = view_begin;
+    L.view_count = view_count;
+    L.amplitude = opts ? opts->amplitude : 1;
+    L.accumulate = accumulate;
+    CVPB_CUDA(cvpb::launch_tt(L, false, static_cast<cudaStream_t>(stream)));
+    return CVPB_OK;
+}
+
+// ---- vector ops -------------------------------------------------------------------
+
+int cvpb_vec_dot(cvpb_context* ctx, const float* a, const float* b, size_t n, double* out_host,
+                 void* stream) {
+    CVPB_TRY(check_ctx(ctx, false));
+    if (!out_host) return fail(CVPB_INVALID_ARGUMENT, "null output");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int np = cvpb::dot_partials_count();
+    CVPB_CUDA(cvpb::launch_dot(a, b, n, ctx->d_partials.p, np, st));
+    std::vector<double> h(np);
+    CVPB_CUDA(cudaMemcpyAsync(h.data(), ctx->d_partials.p, sizeof(double) * np,
+                              cudaMemcpyDeviceToHost, st));
+    CVPB_CUDA(cudaStreamSynchronize(st));
+    double sum = 0.0, c = 0.0;
+    for (double x : h) {
+        const double y = x - c;
+        const double t = sum + y;
+        c = (t - sum) - y;
+        sum = t;
+    }
+    *out_host = sum;
+    return CVPB_OK;
+}
+
+int cvpb_vec_axpy(cvpb_context* ctx, double alpha, const float* x, float* y, size_t n, void* stream) {
+    CVPB_TRY(check_ctx(ctx, false));
+    CVPB_CUDA(cvpb::launch_axpy(alpha, x, y, n, static_cast<cudaStream_t>(stream)));
+    return CVPB_OK;
+}
+
+int cvpb_vec_xpby(cvpb_context* ctx, const float* s, double beta, float* p, size_t n, void* stream) {
+    CVPB_TRY(check_ctx(ctx, false));
+    CVPB_CUDA(cvpb::launch_xpby(s, beta, p, n, static_cast<cudaStream_t>(stream)));
+    return CVPB_OK;
+}
+
+int cvpb_vec_all_finite(cvpb_context* ctx, const float* x, size_t n, int* out_host, void* stream) {
+    CVPB_TRY(check_ctx(ctx, false));
+    if (!out_host) return fail(CVPB_INVALID_ARGUMENT, "null output");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int one = 1;
+    CVPB_CUDA(cudaMemcpyAsync(ctx->d_flag.p, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    CVPB_CUDA(cvpb::launch_all_finite(x, n, ctx->d_flag.p, st));
+    int h = 1;
+    CVPB_CUDA(cudaMemcpyAsync(&h, ctx->d_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CVPB_CUDA(cudaStreamSynchronize(st));
+    *out_host = h;
+    return CVPB_OK;
+}
+
+// ---- device-resident CGLS (solver.cpp:55-106) ------------------------------------
+
+int cvpb_cgls(cvpb_context* ctx, int projector, const cvpb_cvp_options* cvp_opts, int k_per_edge,
+              const float* d_b, float* d_x, int iterations, double* residual_norms, void* stream) {
+    CVPB_TRY(check_ctx(ctx));
+    if (iterations < 1) return fail(CVPB_INVALID_ARGUMENT, "cgls needs at least one iteration");
+    if (!d_b || !d_x || !residual_norms) return fail(CVPB_INVALID_ARGUMENT, "null argument");
+    if (projector < 0 || projector > 2) return fail(CVPB_INVALID_ARGUMENT, "unknown projector");
+    cvpb_cvp_options defaults{CVPB_SCALING_EXACT, 1, CVPB_PRECISION_EXACT, CVPB_R_CUT_CENTROID};
+    const cvpb_cvp_options* opts = cvp_opts ? cvp_opts : &defaults;
+    cvpb_exec_policy ex{0, 0, 1};
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t n = ctx->nvox(), m = ctx->npx_view() * ctx->views.size();
+    const int V = int(ctx->views.size());
+    CVPB_CUDA(ctx->cg_r.reserve(m));
+    CVPB_CUDA(ctx->cg_q.reserve(m));
+    CVPB_CUDA(ctx->cg_s.reserve(n));
+    CVPB_CUDA(ctx->cg_p.reserve(n));
+    float *r = ctx->cg_r.p, *q = ctx->cg_q.p, *s = ctx->cg_s.p, *p = ctx->cg_p.p;
+    auto forward = [&](const float* x, float* out) -> int {
+        if (projector == 0) return cvpb_project_cvp(ctx, opts, &ex, x, out, 0, V, st);
+        if (projector == 1) return cvpb_project_siddon(ctx, k_per_edge, nullptr, &ex, x, out, 0, V, st);
+        return cvpb_project_tt(ctx, nullptr, x, out, 0, V, st);
+    };
+    auto adjoint = [&](const float* b, float* out) -> int {
+        if (projector == 0) return cvpb_backproject_cvp(ctx, opts, &ex, b, out, 0, V, 0, st);
+        if (projector == 1) return cvpb_backproject_siddon(ctx, k_per_edge, &ex, b, out, 0, V, 0, st);
+        return cvpb_backproject_tt(ctx, nullptr, b, out, 0, V, 0, st);
+    };
+    auto dotv = [&](const float* a, const float* b, size_t len, double* out) {
+        return cvpb_vec_dot(ctx, a, b, len, out, st);
+    };
+    CVPB_CUDA(cudaMemcpyAsync(r, d_b, sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+    CVPB_CUDA(cudaMemsetAsync(d_x, 0, sizeof(float) * n, st));
+    double rr;
+    CVPB_TRY(dotv(r, r, m, &rr));
+    residual_norms[0] = std::sqrt(rr);
+    CVPB_TRY(adjoint(r, s));
+    CVPB_CUDA(cudaMemcpyAsync(p, s, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+    double gamma;
+    CVPB_TRY(dotv(s, s, n, &gamma));
+    for (int it = 1; it <= iterations; ++it) {
+        if (gamma == 0.0) {  // normal equations satisfied: keep the history flat
+            residual_norms[it] = residual_norms[it - 1];
+            continue;
+        }
+        CVPB_TRY(forward(p, q));
+        double qq;
+        CVPB_TRY(dotv(q, q, m, &qq));
+        if (qq == 0.0)
+            return fail(CVPB_RUNTIME_ERROR,
+                        "CGLS breakdown (A p = 0) at iteration " + std::to_string(it));
+        const double alpha = gamma / qq;
+        CVPB_CUDA(cvpb::launch_axpy(alpha, p, d_x, n, st));
+        CVPB_CUDA(cvpb::launch_axpy(-alpha, q, r, m, st));
+        CVPB_TRY(adjoint(r, s));
+        double gamma_new;
+        CVPB_TRY(dotv(s, s, n, &gamma_new));
+        const double beta = gamma_new / gamma;
+        CVPB_CUDA(cvpb::launch_xpby(s, beta, p, n, st));
+        gamma = gamma_new;
+        int fx = 1, fr = 1;
+        CVPB_TRY(cvpb_vec_all_finite(ctx, d_x, n, &fx, st));
+        CVPB_TRY(cvpb_vec_all_finite(ctx, r, m, &fr, st));
+        if (!fx || !fr)
+            return fail(CVPB_RUNTIME_ERROR,
+                        "CGLS diverged (non-finite iterate) at iteration " + std::to_string(it));
+        CVPB_TRY(dotv(r, r, m, &rr));
+        residual_norms[it] = std::sqrt(rr);
+    }
+    return CVPB_OK;
+}
+
+}  // extern "C"

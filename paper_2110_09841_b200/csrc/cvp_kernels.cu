@@ -1,0 +1,519 @@
+// CVP forward (scatter) and backward (gather) kernels for sm_100a.
+//
+// Reference: /root/reference/proj/src/cvp.cpp forward_view (:357-412),
+// backward_view (:414-458), project/backproject_cvp_impl (:460-500).
+//
+// Work decomposition: one CTA owns a brick of
+// BI x BJ voxel columns x BK voxels along x3 and loops over its views.
+// Per view:
+//   G-phase  one thread per column computes that column's cuts (float64 in
+//            exact mode) into shared memory; warp 0 computes the brick's
+//            detector footprint rectangle;
+//   V-phase  warp w walks columns w, w+8, ...; lane = voxel k in the brick;
+//            each (voxel, cut, row) record is
+//              forward:  atomically added into a shared-memory detector tile
+//                        (column-major, conflict-free for consecutive rows),
+//              backward: gathered from a shared-memory copy of the scaled
+//                        image footprint (no atomics);
+//   flush    forward: the tile is added to HBM with one coalesced float atomic
+//            per touched pixel, multiplied by the phase-2 pixel scale
+//            (cvp.cpp:473-474) on the way out.
+// The brick's attenuation values (forward) / accumulators (backward) stay in
+// shared memory across all views, so HBM sees the volume once per launch.
+#include <algorithm>
+#include <cstdio>
+
+#include "cvp_device.cuh"
+#include "kernels.hpp"
+
+namespace cvpb {
+
+namespace {
+
+constexpr int BI = 16, BJ = 16, BK = 32;
+constexpr int NCOL = BI * BJ;           // 256 columns per brick
+constexpr int NT = 256;                 // threads per CTA
+constexpr int NWARP = NT / 32;
+constexpr int MAXC = 4;                 // cuts cached per column; more are recomputed
+constexpr int MUS = BK + 1;             // padded column stride of the voxel tile
+
+struct CvpParams {
+    Scene sc;
+    const ViewConst* views;
+    const float* scales;      // [slots][rows*cols]
+    const float* vol_in;      // forward input
+    float* vol_out;           // backward output
+    const float* proj_in;     // backward input (view_begin-relative)
+    float* proj_out;          // forward output (view_begin-relative)
+    int view_begin, view_count, views_per_group;
+    int corr, per_row_r;
+    int tile_cap;
+    int accumulate;           // backward: add into vol_out
+    int atomic_out;           // backward: several view groups -> atomicAdd
+    int* err;
+};
+
+// Shared-memory layout (dynamic).
+struct Smem {
+    // cut cache, SoA [MAXC][NCOL]
+    double q[MAXC * NCOL];
+    int n[MAXC * NCOL];
+    float g[MAXC * NCOL], A[MAXC * NCOL], rho2[MAXC * NCOL], bh[MAXC * NCOL];
+    float halfw[MAXC * NCOL], dd[MAXC * NCOL], d0[MAXC * NCOL];
+    int count[NCOL];
+    float rho2c[NCOL];
+    int nz[NCOL];             // forward: column has a nonzero voxel in the brick
+    float vox[NCOL * MUS];    // forward: mu; backward: accumulators
+    int tile_m0, tile_n0, tile_rows, tile_cols, tile_stride, tile_ok;
+};
+
+__device__ __forceinline__ void store_cut(Smem& s, int slot, const CutRec& r) {
+    s.n[slot] = r.n;
+    s.q[slot] = r.q;
+    s.g[slot] = r.g;
+    s.A[slot] = r.A;
+    s.rho2[slot] = r.rho2;
+    s.bh[slot] = r.bh;
+    s.halfw[slot] = r.halfw;
+    s.dd[slot] = r.dd;
+    s.d0[slot] = r.d0;
+}
+
+__device__ __forceinline__ CutRec load_cut(const Smem& s, int slot) {
+    CutRec r;
+    r.n = s.n[slot];
+    r.q = s.q[slot];
+    r.g = s.g[slot];
+    r.A = s.A[slot];
+    r.rho2 = s.rho2[slot];
+    r.bh = s.bh[slot];
+    r.halfw = s.halfw[slot];
+    r.dd = s.dd[slot];
+    r.d0 = s.d0[slot];
+    return r;
+}
+
+// Detector rectangle that contains every record a voxel of the brick can
+// emit under view vc: chi1 over the brick's base corners; chi2 over its z
+// range and its depth range widened by half a voxel-base diagonal (bound on
+// the elevation rectangle's depth spread |hw|*halfw). One extra pixel of
+// margin absorbs rounding; anything outside still lands correctly through the
+// global fallback path.
+__device__ void brick_footprint(const ViewConst& vc, const Scene& sc, int i0, int i1, int j0,
+                                int j1, int k0, int k1, int& m0, int& m1, int& n0, int& n1) {
+    const double xs[2] = {sc.minx + i0 * sc.a1, sc.minx + i1 * sc.a1};
+    const double ys[2] = {sc.miny + j0 * sc.a2, sc.miny + j1 * sc.a2};
+    double cmin = INFINITY, cmax = -INFINITY, dmin = INFINITY, dmax = -INFINITY;
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) {
+            const double px = xs[a] - vc.sx, py = ys[b] - vc.sy;
+            const double d = vc.w3x * px + vc.w3y * py;
+            const double c1 = (vc.w1x * px + vc.w1y * py) / d;
+            cmin = fmin(cmin, c1);
+            cmax = fmax(cmax, c1);
+            dmin = fmin(dmin, d);
+            dmax = fmax(dmax, d);
+        }
+    const double margin = 0.5 * sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2);
+    dmin -= margin;
+    dmax += margin;
+    const double zs[2] = {sc.minz + k0 * sc.a3 - vc.s3, sc.minz + k1 * sc.a3 - vc.s3};
+    double rmin = INFINITY, rmax = -INFINITY;
+    if (!(dmin > 0.0)) {
+        m0 = 1;
+        m1 = 0;
+        return;
+    }
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) {
+            const double d = b ? dmax : dmin;
+            const double c2 = vc.pp2 - zs[a] * vc.f_over_b2 / d;
+            rmin = fmin(rmin, c2);
+            rmax = fmax(rmax, c2);
+        }
+    n0 = max(int(ceil(cmin - 0.5)) - 1, 0);
+    n1 = min(int(floor(cmax + 0.5)) + 1, sc.cols - 1);
+    m0 = max(int(ceil(rmin - 0.5)) - 1, 0);
+    m1 = min(int(floor(rmax + 0.5)) + 1, sc.rows - 1);
+}
+
+template <bool EXACT, bool FWD>
+__global__ void __launch_bounds__(NT, 2) cvp_brick_kernel(CvpParams p) {
+    using G = typename std::conditional<EXACT, double, float>::type;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+    float* tile = reinterpret_cast<float*>(smem_raw + sizeof(Smem));
+
+    const Scene& sc = p.sc;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nbi = (sc.n1 + BI - 1) / BI, nbj = (sc.n2 + BJ - 1) / BJ;
+    int b = blockIdx.x;
+    const int bi = b % nbi;
+    b /= nbi;
+    const int bj = b % nbj;
+    const int bk = b / nbj;
+    const int i0 = bi * BI, j0 = bj * BJ, k0 = bk * BK;
+    const int i1 = min(i0 + BI, sc.n1), j1 = min(j0 + BJ, sc.n2), k1 = min(k0 + BK, sc.n3);
+
+    const int vg0 = p.view_begin + blockIdx.y * p.views_per_group;
+    const int vg1 = min(vg0 + p.views_per_group, p.view_begin + p.view_count);
+    if (vg0 >= vg1) return;
+
+    const size_t plane = size_t(sc.n1) * sc.n2;
+    // Stage the brick's voxels: [column][k] with odd stride (bank-conflict free).
+    if (tid < NCOL) s.nz[tid] = 0;
+    __syncthreads();
+    for (int idx = tid; idx < NCOL * BK; idx += NT) {
+        const int kk = idx / NCOL, c = idx % NCOL;
+        const int i = i0 + (c % BI), j = j0 + (c / BI), k = k0 + kk;
+        float val = 0.f;
+        if (FWD && i < i1 && j < j1 && k < k1) {
+            val = __ldg(p.vol_in + size_t(k) * plane + size_t(j) * sc.n1 + i);
+            if (val != 0.f) s.nz[c] = 1;
+        }
+        s.vox[c * MUS + kk] = val;
+    }
+
+    const int rows = sc.rows, cols = sc.cols;
+    const size_t npx = size_t(rows) * cols;
+    const float h = float(0.5 * sc.a3);
+    const bool corr = p.corr != 0, per_row_r = p.per_row_r != 0;
+    const int k = k0 + lane;
+    const bool kvalid = k < k1;
+    const double zc64 = sc.minz + (k + 0.5) * sc.a3;
+
+    for (int v = vg0; v < vg1; ++v) {
+        const ViewConst& vc = p.views[v];
+        __syncthreads();  // previous view's V-phase / flush is complete
+        // ---- G-phase: column cuts --------------------------------------
+        {
+            const int c = tid;
+            const int i = i0 + (c % BI), j = j0 + (c / BI);
+            int cnt = 0;
+            if (i < i1 && j < j1 && (!FWD || s.nz[c])) {
+                const ViewG<G> vgm = load_view_g<G>(vc);
+                float rc;
+                cnt = visit_column_cuts<G>(vc, vgm, sc, i, j, true, corr, &rc,
+                                           [&](const CutRec& r) {
+                                               if (cnt < MAXC) store_cut(s, cnt * NCOL + c, r);
+                                               ++cnt;
+                                           });
+                if (cnt < 0) {
+                    atomicOr(p.err, cnt == -1 ? kDevSourcePlane : kDevDegenerate);
+                    cnt = 0;
+                }
+                s.rho2c[c] = rc;
+            }
+            s.count[c] = cnt;
+        }
+        if (tid == 0) {
+            int m0, m1, n0, n1;
+            brick_footprint(vc, sc, i0, i1, j0, j1, k0, k1, m0, m1, n0, n1);
+            const int tr = max(m1 - m0 + 1, 0), tc = max(n1 - n0 + 1, 0);
+            const int stride = tr | 1;
+            s.tile_m0 = m0;
+            s.tile_n0 = n0;
+            s.tile_rows = tr;
+            s.tile_cols = tc;
+            s.tile_stride = stride;
+            s.tile_ok = (tr > 0 && tc > 0 && stride * tc <= p.tile_cap) ? 1 : 0;
+        }
+        __syncthreads();
+        const int tm0 = s.tile_m0, tn0 = s.tile_n0, trows = s.tile_rows, tcols = s.tile_cols;
+        const int tstride = s.tile_stride;
+        const bool tile_ok = s.tile_ok != 0;
+        const float* scale = p.scales + size_t(vc.scale_slot) * npx;
+        const size_t vloc = size_t(v - p.view_begin);
+        // ---- tile prologue ----------------------------------------------
+        if (tile_ok) {
+            const int ntile = trows * tcols;
+            if (FWD) {
+                for (int idx = tid; idx < tstride * tcols; idx += NT) tile[idx] = 0.f;
+            } else {
+                const float* img = p.proj_in + vloc * npx;
+                for (int idx = tid; idx < ntile; idx += NT) {
+                    const int r = idx / tcols, cc = idx % tcols;
+                    const size_t px = size_t(tm0 + r) * cols + (tn0 + cc);
+                    tile[cc * tstride + r] = __ldg(img + px) * __ldg(scale + px);
+                }
+            }
+            __syncthreads();
+        }
+        // ---- V-phase -----------------------------------------------------
+        const double dz64 = zc64 - vc.s3;
+        const float dz = EXACT ? float(dz64) : float(zc64) - float(vc.s3);
+        const double pp2 = vc.pp2;
+        const float fb2 = float(vc.f_over_b2);
+        float* out_img = FWD ? p.proj_out + vloc * npx : nullptr;
+        const float* in_img = FWD ? nullptr : p.proj_in + vloc * npx;
+        for (int c = warp; c < NCOL; c += NWARP) {
+            const int cnt = s.count[c];
+            if (cnt == 0) continue;
+            float mu = 0.f;
+            if (FWD) {
+                mu = s.vox[c * MUS + lane];
+                if (!__any_sync(0xffffffffu, kvalid && mu != 0.f)) continue;
+            }
+            const bool active = kvalid && (!FWD || mu != 0.f);
+            const float inv_r2_fixed = per_row_r ? -1.f : 1.f / (s.rho2c[c] + dz * dz);
+            float acc = 0.f;
+            auto emit = [&](int m, int n, float vol, float inv_r2) {
+                const float w = vol * inv_r2;
+                const int r = m - tm0, cc = n - tn0;
+                const bool in_tile = tile_ok && unsigned(r) < unsigned(trows) &&
+                                     unsigned(cc) < unsigned(tcols);
+                if (FWD) {
+                    if (in_tile) {
+                        atomicAdd(&tile[cc * tstride + r], mu * w);
+                    } else {
+                        const size_t px = size_t(m) * cols + n;
+                        atomicAdd(out_img + px, mu * w * __ldg(scale + px));
+                    }
+                } else {
+                    if (in_tile) {
+                        acc += tile[cc * tstride + r] * w;
+                    } else {
+                        const size_t px = size_t(m) * cols + n;
+                        acc += __ldg(in_img + px) * __ldg(scale + px) * w;
+                    }
+                }
+            };
+            auto do_cut = [&](const CutRec& r) {
+                const bool corrected = corr && r.halfw > 0.f && dz * dz > r.rho2 * 1e-28f;
+                const double ck = voxel_anchor<EXACT>(pp2, dz64, dz, r);
+                walk_rows<true>(r, ck, pp2, fb2, dz, h, corrected, per_row_r, inv_r2_fixed, rows,
+                                emit);
+            };
+            if (active) {
+                const int ncached = min(cnt, MAXC);
+                for (int q = 0; q < ncached; ++q) do_cut(load_cut(s, q * NCOL + c));
+            }
+            if (cnt > MAXC) {
+                // rare overflow (very small pixels vs voxels): recompute cuts >= MAXC
+                const int i = i0 + (c % BI), j = j0 + (c / BI);
+                const ViewG<G> vgm = load_view_g<G>(vc);
+                float rc;
+                int idx = 0;
+                visit_column_cuts<G>(vc, vgm, sc, i, j, true, corr, &rc, [&](const CutRec& r) {
+                    if (idx++ >= MAXC && active) do_cut(r);
+                });
+            }
+            if (!FWD && kvalid) s.vox[c * MUS + lane] += acc;
+        }
+        // ---- flush (forward) ----------------------------------------------
+        if (FWD && tile_ok) {
+            __syncthreads();
+            const int ntile = trows * tcols;
+            for (int idx = tid; idx < ntile; idx += NT) {
+                const int r = idx / tcols, cc = idx % tcols;
+                const float val = tile[cc * tstride + r];
+                if (val != 0.f) {
+                    const size_t px = size_t(tm0 + r) * cols + (tn0 + cc);
+                    atomicAdd(out_img + px, val * __ldg(scale + px));
+                }
+            }
+        }
+    }
+    if (!FWD) {
+        __syncthreads();
+        for (int idx = tid; idx < NCOL * BK; idx += NT) {
+            const int kk = idx / NCOL, c = idx % NCOL;
+            const int i = i0 + (c % BI), j = j0 + (c / BI), kq = k0 + kk;
+            if (i < i1 && j < j1 && kq < k1) {
+                float* dst = p.vol_out + size_t(kq) * plane + size_t(j) * sc.n1 + i;
+                const float val = s.vox[c * MUS + kk];
+                if (p.atomic_out)
+                    atomicAdd(dst, val);
+                else if (p.accumulate)
+                    *dst += val;
+                else
+                    *dst = val;
+            }
+        }
+    }
+}
+
+// Per-pixel phase-2 factors (ScaleCache, cvp.cpp:264-302) in float64, stored
+// as float32. Exact mode: 1/solid angle of the pixel seen from the source,
+// evaluated as two Van Oosterom–Strackee triangles (cancellation-free; the
+// reference's 2*pi - sum(acos) form carries ~1e-8 relative noise at C-arm
+// pixel sizes). Cos mode: f^2 / (b1 b2 cos^3 theta) (cvp.cpp:288-292).
+__device__ double tri_solid_angle(const double* a, const double* b, const double* c) {
+    const double cx = b[1] * c[2] - b[2] * c[1];
+    const double cy = b[2] * c[0] - b[0] * c[2];
+    const double cz = b[0] * c[1] - b[1] * c[0];
+    const double num = fabs(a[0] * cx + a[1] * cy + a[2] * cz);
+    const double den = 1.0 + (a[0] * b[0] + a[1] * b[1] + a[2] * b[2]) +
+                       (b[0] * c[0] + b[1] * c[1] + b[2] * c[2]) +
+                       (c[0] * a[0] + c[1] * a[1] + c[2] * a[2]);
+    return 2.0 * atan2(num, den);
+}
+
+__global__ void scale_image_kernel(double f, double pp1, double pp2, double b1, double b2, int rows,
+                                   int cols, int exact, float* out, double* out64) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= rows * cols) return;
+    const int m = idx / cols, n = idx % cols;
+    double s;
+    if (!exact) {
+        const double u = (n - pp1) * b1, w = (m - pp2) * b2;
+        const double c = f / sqrt(u * u + w * w + f * f);
+        s = f * f / (b1 * b2 * c * c * c);
+    } else {
+        const double u0 = (n - 0.5 - pp1) * b1, u1 = (n + 0.5 - pp1) * b1;
+        const double w0 = (m - 0.5 - pp2) * b2, w1 = (m + 0.5 - pp2) * b2;
+        double t[4][3] = {{u0, w0, f}, {u1, w0, f}, {u1, w1, f}, {u0, w1, f}};
+        for (int q = 0; q < 4; ++q) {
+            const double l = 1.0 / sqrt(t[q][0] * t[q][0] + t[q][1] * t[q][1] + t[q][2] * t[q][2]);
+            t[q][0] *= l;
+            t[q][1] *= l;
+            t[q][2] *= l;
+        }
+        const double omega = tri_solid_angle(t[0], t[1], t[2]) + tri_solid_angle(t[0], t[2], t[3]);
+        s = 1.0 / omega;
+    }
+    if (out) out[idx] = float(s);
+    if (out64) out64[idx] = s;
+}
+
+// Single-voxel record dump through the device kernel's own geometry code
+// (the bookkeeping view of collect_cut_records, cvp.cpp:652-689).
+template <bool EXACT>
+__global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, int i, int j, int k,
+                                   int corr_opt, int per_row_r, int clamp, int cap, int* rows_out,
+                                   int* cols_out, double* vol_out, double* inv_out, int* n_out,
+                                   int* err) {
+    using G = typename std::conditional<EXACT, double, float>::type;
+    const ViewConst vc = views[view];
+    const ViewG<G> vgm = load_view_g<G>(vc);
+    const double zc64 = sc.minz + (k + 0.5) * sc.a3;
+    const double dz64 = zc64 - vc.s3;
+    const float dz = EXACT ? float(dz64) : float(zc64) - float(vc.s3);
+    const float h = float(0.5 * sc.a3);
+    const bool corr = corr_opt != 0;
+    int count = 0;
+    float rc;
+    auto emit = [&](int m, int n, float vol, float inv_r2) {
+        if (count < cap) {
+            rows_out[count] = m;
+            cols_out[count] = n;
+            vol_out[count] = vol;
+            inv_out[count] = inv_r2;
+        }
+        ++count;
+    };
+    // first pass only gets rho2c
+    const int st = visit_column_cuts<G>(vc, vgm, sc, i, j, clamp != 0, corr, &rc,
+                                        [&](const CutRec&) {});
+    if (st < 0) {
+        *err = st == -1 ? kDevSourcePlane : kDevDegenerate;
+        *n_out = 0;
+        return;
+    }
+    const float inv_r2_fixed = per_row_r ? -1.f : 1.f / (rc + dz * dz);
+    visit_column_cuts<G>(vc, vgm, sc, i, j, clamp != 0, corr, &rc, [&](const CutRec& r) {
+        const bool corrected = corr && r.halfw > 0.f && dz * dz > r.rho2 * 1e-28f;
+        const double ck = voxel_anchor<EXACT>(vc.pp2, dz64, dz, r);
+        if (clamp)
+            walk_rows<true>(r, ck, vc.pp2, float(vc.f_over_b2), dz, h, corrected, per_row_r != 0,
+                            inv_r2_fixed, sc.rows, emit);
+        else
+            walk_rows<false>(r, ck, vc.pp2, float(vc.f_over_b2), dz, h, corrected, per_row_r != 0,
+                             inv_r2_fixed, sc.rows, emit);
+    });
+    *n_out = count;
+}
+
+template <bool EXACT, bool FWD> cudaError_t setup_kernel(int dyn_smem) {
+    return cudaFuncSetAttribute(cvp_brick_kernel<EXACT, FWD>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
+}
+
+}  // namespace
+
+int cvp_tile_cap_floats() { return 6144; }
+
+cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
+    const Scene& sc = L.sc;
+    if (L.view_count <= 0) return cudaSuccess;
+    const int tile_cap = cvp_tile_cap_floats();
+    const int dyn = int(sizeof(Smem)) + tile_cap * int(sizeof(float));
+    const int nbricks = ((sc.n1 + BI - 1) / BI) * ((sc.n2 + BJ - 1) / BJ) * ((sc.n3 + BK - 1) / BK);
+    // Enough CTAs to fill 148 SMs x 2 resident: split views into groups when
+    // the volume has few bricks (c1: 32 bricks). Deterministic mode keeps one
+    // group so the backward accumulation order is fixed.
+    int groups = 1;
+    const int target = 148 * 2 * 2;
+    if (!L.deterministic && nbricks < target) groups = std::min(L.view_count, (target + nbricks - 1) / nbricks);
+    const int per = (L.view_count + groups - 1) / groups;
+    groups = (L.view_count + per - 1) / per;
+
+    CvpParams p;
+    p.sc = sc;
+    p.views = L.views;
+    p.scales = L.scales;
+    p.vol_in = L.vol_in;
+    p.vol_out = L.vol_out;
+    p.proj_in = L.proj_in;
+    p.proj_out = L.proj_out;
+    p.view_begin = L.view_begin;
+    p.view_count = L.view_count;
+    p.views_per_group = per;
+    p.corr = L.elevation_correction;
+    p.per_row_r = L.cut_centroid;
+    p.tile_cap = tile_cap;
+    p.accumulate = L.accumulate;
+    p.atomic_out = groups > 1 ? 1 : 0;
+    p.err = L.err;
+
+    cudaError_t e;
+    if (!L.forward && groups > 1 && !L.accumulate) {
+        e = cudaMemsetAsync(L.vol_out, 0, sizeof(float) * size_t(sc.n1) * sc.n2 * sc.n3, stream);
+        if (e != cudaSuccess) return e;
+    }
+    dim3 grid(nbricks, groups);
+    if (L.forward) {
+        e = cudaMemsetAsync(L.proj_out, 0, sizeof(float) * size_t(sc.rows) * sc.cols * L.view_count,
+                            stream);
+        if (e != cudaSuccess) return e;
+        if (L.exact) {
+            if ((e = setup_kernel<true, true>(dyn)) != cudaSuccess) return e;
+            cvp_brick_kernel<true, true><<<grid, NT, dyn, stream>>>(p);
+        } else {
+            if ((e = setup_kernel<false, true>(dyn)) != cudaSuccess) return e;
+            cvp_brick_kernel<false, true><<<grid, NT, dyn, stream>>>(p);
+        }
+    } else {
+        if (L.exact) {
+            if ((e = setup_kernel<true, false>(dyn)) != cudaSuccess) return e;
+            cvp_brick_kernel<true, false><<<grid, NT, dyn, stream>>>(p);
+        } else {
+            if ((e = setup_kernel<false, false>(dyn)) != cudaSuccess) return e;
+            cvp_brick_kernel<false, false><<<grid, NT, dyn, stream>>>(p);
+        }
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scale_image(double f, double pp1, double pp2, double b1, double b2, int rows,
+                               int cols, int exact, float* out, double* out64, cudaStream_t stream) {
+    const int n = rows * cols;
+    scale_image_kernel<<<(n + 255) / 256, 256, 0, stream>>>(f, pp1, pp2, b1, b2, rows, cols, exact,
+                                                           out, out64);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cut_records(const Scene& sc, const ViewConst* views, int view, int i, int j,
+                               int k, int exact, int corr, int per_row_r, int clamp, int cap,
+                               int* rows, int* cols, double* vol, double* inv, int* n_out, int* err,
+                               cudaStream_t stream) {
+    if (exact)
+        cut_records_kernel<true><<<1, 1, 0, stream>>>(sc, views, view, i, j, k, corr, per_row_r,
+                                                      clamp, cap, rows, cols, vol, inv, n_out, err);
+    else
+        cut_records_kernel<false><<<1, 1, 0, stream>>>(sc, views, view, i, j, k, corr, per_row_r,
+                                                       clamp, cap, rows, cols, vol, inv, n_out, err);
+    return cudaGetLastError();
+}
+
+}  // namespace cvpb

@@ -1,0 +1,73 @@
+// Host-side launch interfaces of the device kernels (internal to libcvpb200).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "common.cuh"
+
+namespace cvpb {
+
+struct CvpLaunch {
+    Scene sc;
+    const ViewConst* views;   // device, all views of the scene
+    const float* scales;      // device, [slots][rows*cols] (mode already selected)
+    const float* vol_in;
+    float* vol_out;
+    const float* proj_in;
+    float* proj_out;
+    int view_begin, view_count;
+    int forward, exact, elevation_correction, cut_centroid;
+    int accumulate, deterministic;
+    int* err;                 // device error flag
+};
+
+int cvp_tile_cap_floats();
+cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream);
+cudaError_t launch_scale_image(double f, double pp1, double pp2, double b1, double b2, int rows,
+                               int cols, int exact, float* out, double* out64, cudaStream_t stream);
+cudaError_t launch_cut_records(const Scene& sc, const ViewConst* views, int view, int i, int j,
+                               int k, int exact, int corr, int per_row_r, int clamp, int cap,
+                               int* rows, int* cols, double* vol, double* inv, int* n_out, int* err,
+                               cudaStream_t stream);
+
+struct SiddonLaunch {
+    Scene sc;
+    const ViewConst* views;
+    const float* vol_in;
+    float* vol_out;
+    const float* proj_in;
+    float* proj_out;
+    int view_begin, view_count;
+    int k_per_edge;
+    int r0, r1, c0, c1;       // forward ROI (resolved, half-open)
+    const int* d_box;         // forward: device {lo0,lo1,lo2,hi0,hi1,hi2} of nonzero voxels
+    int accumulate;
+};
+cudaError_t launch_siddon(const SiddonLaunch& L, bool forward, cudaStream_t stream);
+cudaError_t launch_nonzero_box(const float* vol, const Scene& sc, int* d_box6, cudaStream_t stream);
+
+struct TTLaunch {
+    Scene sc;
+    const ViewConst* views;
+    const float* vol_in;
+    float* vol_out;
+    const float* proj_in;
+    float* proj_out;
+    int view_begin, view_count;
+    int amplitude;
+    int accumulate;
+};
+cudaError_t launch_tt(const TTLaunch& L, bool forward, cudaStream_t stream);
+
+// vector ops (CGLS)
+cudaError_t launch_dot(const float* a, const float* b, size_t n, double* d_partials,
+                       int n_partials, cudaStream_t stream);
+int dot_partials_count();
+cudaError_t launch_axpy(double alpha, const float* x, float* y, size_t n, cudaStream_t stream);
+cudaError_t launch_xpby(const float* s, double beta, float* p, size_t n, cudaStream_t stream);
+cudaError_t launch_all_finite(const float* x, size_t n, int* d_flag, cudaStream_t stream);
+cudaError_t launch_f64_to_f32(const double* in, float* out, size_t n, cudaStream_t stream);
+cudaError_t launch_f32_to_f64(const float* in, double* out, size_t n, cudaStream_t stream);
+
+}  // namespace cvpb

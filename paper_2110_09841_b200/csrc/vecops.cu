@@ -1,0 +1,133 @@
+// Device-resident vector operations for CGLS (solver.cpp:15-106): compensated
+// float64 dot products of float32 vectors, axpy / xpby updates and the finite
+// check. All are HBM-streaming kernels sized as a multiple of the 148 SMs.
+#include <cmath>
+
+#include "kernels.hpp"
+
+namespace cvpb {
+
+namespace {
+
+constexpr int kDotBlocks = 148 * 4;
+constexpr int kThreads = 256;
+
+// Per-thread Kahan accumulation of exact float32 x float32 products in
+// float64 (dot_kahan, solver.cpp:15-24), then a pairwise block reduction.
+__global__ void dot_kernel(const float* __restrict__ a, const float* __restrict__ b, size_t n,
+                           double* partials) {
+    double sum = 0.0, c = 0.0;
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    // float4 main body when both pointers are 16-byte aligned
+    const bool vec = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+    if (vec) {
+        const size_t n4 = n / 4;
+        const float4* a4 = reinterpret_cast<const float4*>(a);
+        const float4* b4 = reinterpret_cast<const float4*>(b);
+        for (size_t q = i; q < n4; q += stride) {
+            const float4 x = __ldg(a4 + q), y = __ldg(b4 + q);
+            const double p = double(x.x) * y.x + double(x.y) * y.y + double(x.z) * y.z +
+                             double(x.w) * y.w;
+            const double yk = p - c;
+            const double t = sum + yk;
+            c = (t - sum) - yk;
+            sum = t;
+        }
+        i = n4 * 4 + i;
+    }
+    for (; i < n; i += stride) {
+        const double p = double(a[i]) * double(b[i]);
+        const double yk = p - c;
+        const double t = sum + yk;
+        c = (t - sum) - yk;
+        sum = t;
+    }
+    double v = sum - c;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __shared__ double ws[kThreads / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) s += ws[w];
+        partials[blockIdx.x] = s;
+    }
+}
+
+__global__ void axpy_kernel(double alpha, const float* __restrict__ x, float* __restrict__ y,
+                            size_t n) {
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+        y[i] = float(double(y[i]) + alpha * double(x[i]));
+}
+
+__global__ void xpby_kernel(const float* __restrict__ s, double beta, float* __restrict__ p,
+                            size_t n) {
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+        p[i] = float(double(s[i]) + beta * double(p[i]));
+}
+
+__global__ void finite_kernel(const float* __restrict__ x, size_t n, int* flag) {
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    bool bad = false;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+        bad |= !isfinite(x[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(flag, 0);
+}
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ in, float* __restrict__ out, size_t n) {
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+        out[i] = float(in[i]);
+}
+
+__global__ void f32_to_f64_kernel(const float* __restrict__ in, double* __restrict__ out, size_t n) {
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+        out[i] = double(in[i]);
+}
+
+inline int grid_for(size_t n) {
+    const size_t blocks = (n + kThreads - 1) / kThreads;
+    return int(blocks < size_t(148 * 16) ? (blocks > 0 ? blocks : 1) : 148 * 16);
+}
+
+}  // namespace
+
+int dot_partials_count() { return kDotBlocks; }
+
+cudaError_t launch_dot(const float* a, const float* b, size_t n, double* d_partials,
+                       int n_partials, cudaStream_t stream) {
+    if (n_partials < kDotBlocks) return cudaErrorInvalidValue;
+    dot_kernel<<<kDotBlocks, kThreads, 0, stream>>>(a, b, n, d_partials);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_axpy(double alpha, const float* x, float* y, size_t n, cudaStream_t stream) {
+    axpy_kernel<<<grid_for(n), kThreads, 0, stream>>>(alpha, x, y, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xpby(const float* s, double beta, float* p, size_t n, cudaStream_t stream) {
+    xpby_kernel<<<grid_for(n), kThreads, 0, stream>>>(s, beta, p, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_all_finite(const float* x, size_t n, int* d_flag, cudaStream_t stream) {
+    finite_kernel<<<grid_for(n), kThreads, 0, stream>>>(x, n, d_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_f64_to_f32(const double* in, float* out, size_t n, cudaStream_t stream) {
+    f64_to_f32_kernel<<<grid_for(n), kThreads, 0, stream>>>(in, out, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_f32_to_f64(const float* in, double* out, size_t n, cudaStream_t stream) {
+    f32_to_f64_kernel<<<grid_for(n), kThreads, 0, stream>>>(in, out, n);
+    return cudaGetLastError();
+}
+
+}  // namespace cvpb
