@@ -53,43 +53,35 @@ struct CvpParams {
     int* err;
 };
 
-// Shared-memory layout (dynamic).
+// Shared-memory layout (dynamic). Cut records are two float4 each so a warp
+// reads one record with two broadcast LDS.128.
 struct Smem {
-    // cut cache, SoA [MAXC][NCOL]
-    double q[MAXC * NCOL];
-    int n[MAXC * NCOL];
-    float g[MAXC * NCOL], A[MAXC * NCOL], rho2[MAXC * NCOL], bh[MAXC * NCOL];
-    float halfw[MAXC * NCOL], dd[MAXC * NCOL], d0[MAXC * NCOL];
-    int count[NCOL];
+    float4 cutA[MAXC * NCOL];  // {A, g, rho2, halfw}
+    float4 cutB[MAXC * NCOL];  // {kc, tr_a, tr_b, n (bits)}
+    double Q0[NCOL];
     float rho2c[NCOL];
+    int count[NCOL];
     int nz[NCOL];             // forward: column has a nonzero voxel in the brick
     float vox[NCOL * MUS];    // forward: mu; backward: accumulators
     int tile_m0, tile_n0, tile_rows, tile_cols, tile_stride, tile_ok;
 };
 
 __device__ __forceinline__ void store_cut(Smem& s, int slot, const CutRec& r) {
-    s.n[slot] = r.n;
-    s.q[slot] = r.q;
-    s.g[slot] = r.g;
-    s.A[slot] = r.A;
-    s.rho2[slot] = r.rho2;
-    s.bh[slot] = r.bh;
-    s.halfw[slot] = r.halfw;
-    s.dd[slot] = r.dd;
-    s.d0[slot] = r.d0;
+    s.cutA[slot] = make_float4(r.A, r.g, r.rho2, r.halfw);
+    s.cutB[slot] = make_float4(r.kc, r.tr_a, r.tr_b, __int_as_float(r.n));
 }
 
 __device__ __forceinline__ CutRec load_cut(const Smem& s, int slot) {
+    const float4 a = s.cutA[slot], b = s.cutB[slot];
     CutRec r;
-    r.n = s.n[slot];
-    r.q = s.q[slot];
-    r.g = s.g[slot];
-    r.A = s.A[slot];
-    r.rho2 = s.rho2[slot];
-    r.bh = s.bh[slot];
-    r.halfw = s.halfw[slot];
-    r.dd = s.dd[slot];
-    r.d0 = s.d0[slot];
+    r.A = a.x;
+    r.g = a.y;
+    r.rho2 = a.z;
+    r.halfw = a.w;
+    r.kc = b.x;
+    r.tr_a = b.y;
+    r.tr_b = b.z;
+    r.n = __float_as_int(b.w);
     return r;
 }
 
@@ -99,8 +91,9 @@ __device__ __forceinline__ CutRec load_cut(const Smem& s, int slot) {
 // the elevation rectangle's depth spread |hw|*halfw). One extra pixel of
 // margin absorbs rounding; anything outside still lands correctly through the
 // global fallback path.
-__device__ void brick_footprint(const ViewConst& vc, const Scene& sc, int i0, int i1, int j0,
-                                int j1, int k0, int k1, int& m0, int& m1, int& n0, int& n1) {
+__host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene& sc, int i0, int i1,
+                                                int j0, int j1, int k0, int k1, int& m0, int& m1,
+                                                int& n0, int& n1) {
     const double xs[2] = {sc.minx + i0 * sc.a1, sc.minx + i1 * sc.a1};
     const double ys[2] = {sc.miny + j0 * sc.a2, sc.miny + j1 * sc.a2};
     double cmin = INFINITY, cmax = -INFINITY, dmin = INFINITY, dmax = -INFINITY;
@@ -117,13 +110,15 @@ __device__ void brick_footprint(const ViewConst& vc, const Scene& sc, int i0, in
     const double margin = 0.5 * sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2);
     dmin -= margin;
     dmax += margin;
-    const double zs[2] = {sc.minz + k0 * sc.a3 - vc.s3, sc.minz + k1 * sc.a3 - vc.s3};
-    double rmin = INFINITY, rmax = -INFINITY;
     if (!(dmin > 0.0)) {
         m0 = 1;
         m1 = 0;
+        n0 = 1;
+        n1 = 0;
         return;
     }
+    const double zs[2] = {sc.minz + k0 * sc.a3 - vc.s3, sc.minz + k1 * sc.a3 - vc.s3};
+    double rmin = INFINITY, rmax = -INFINITY;
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) {
             const double d = b ? dmax : dmin;
@@ -139,7 +134,6 @@ __device__ void brick_footprint(const ViewConst& vc, const Scene& sc, int i0, in
 
 template <bool EXACT, bool FWD>
 __global__ void __launch_bounds__(NT, 2) cvp_brick_kernel(CvpParams p) {
-    using G = typename std::conditional<EXACT, double, float>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
     float* tile = reinterpret_cast<float*>(smem_raw + sizeof(Smem));
@@ -191,18 +185,17 @@ __global__ void __launch_bounds__(NT, 2) cvp_brick_kernel(CvpParams p) {
             const int i = i0 + (c % BI), j = j0 + (c / BI);
             int cnt = 0;
             if (i < i1 && j < j1 && (!FWD || s.nz[c])) {
-                const ViewG<G> vgm = load_view_g<G>(vc);
-                float rc;
-                cnt = visit_column_cuts<G>(vc, vgm, sc, i, j, true, corr, &rc,
-                                           [&](const CutRec& r) {
-                                               if (cnt < MAXC) store_cut(s, cnt * NCOL + c, r);
-                                               ++cnt;
-                                           });
+                ColumnRec col;
+                cnt = column_cuts<EXACT>(vc, sc, i, j, true, corr, col, [&](const CutRec& r) {
+                    if (cnt < MAXC) store_cut(s, cnt * NCOL + c, r);
+                    ++cnt;
+                });
                 if (cnt < 0) {
-                    atomicOr(p.err, cnt == -1 ? kDevSourcePlane : kDevDegenerate);
+                    atomicOr(p.err, kDevSourcePlane);
                     cnt = 0;
                 }
-                s.rho2c[c] = rc;
+                s.Q0[c] = col.Q0;
+                s.rho2c[c] = col.rho2c;
             }
             s.count[c] = cnt;
         }
@@ -240,10 +233,10 @@ __global__ void __launch_bounds__(NT, 2) cvp_brick_kernel(CvpParams p) {
             __syncthreads();
         }
         // ---- V-phase -----------------------------------------------------
+        const double pp2 = vc.pp2;
         const double dz64 = zc64 - vc.s3;
         const float dz = EXACT ? float(dz64) : float(zc64) - float(vc.s3);
-        const double pp2 = vc.pp2;
-        const float fb2 = float(vc.f_over_b2);
+        const float dz2 = dz * dz;
         float* out_img = FWD ? p.proj_out + vloc * npx : nullptr;
         const float* in_img = FWD ? nullptr : p.proj_in + vloc * npx;
         for (int c = warp; c < NCOL; c += NWARP) {
@@ -255,46 +248,49 @@ __global__ void __launch_bounds__(NT, 2) cvp_brick_kernel(CvpParams p) {
                 if (!__any_sync(0xffffffffu, kvalid && mu != 0.f)) continue;
             }
             const bool active = kvalid && (!FWD || mu != 0.f);
-            const float inv_r2_fixed = per_row_r ? -1.f : 1.f / (s.rho2c[c] + dz * dz);
+            int m_ref;
+            float u0, pm;
+            voxel_anchor<EXACT>(pp2, dz64, dz, s.Q0[c], m_ref, u0, pm);
+            const float inv_r2_fixed = per_row_r ? -1.f : fast_rcp(s.rho2c[c] + dz2);
             float acc = 0.f;
-            auto emit = [&](int m, int n, float vol, float inv_r2) {
-                const float w = vol * inv_r2;
-                const int r = m - tm0, cc = n - tn0;
-                const bool in_tile = tile_ok && unsigned(r) < unsigned(trows) &&
-                                     unsigned(cc) < unsigned(tcols);
-                if (FWD) {
-                    if (in_tile) {
-                        atomicAdd(&tile[cc * tstride + r], mu * w);
-                    } else {
-                        const size_t px = size_t(m) * cols + n;
-                        atomicAdd(out_img + px, mu * w * __ldg(scale + px));
-                    }
-                } else {
-                    if (in_tile) {
-                        acc += tile[cc * tstride + r] * w;
-                    } else {
-                        const size_t px = size_t(m) * cols + n;
-                        acc += __ldg(in_img + px) * __ldg(scale + px) * w;
-                    }
-                }
-            };
             auto do_cut = [&](const CutRec& r) {
-                const bool corrected = corr && r.halfw > 0.f && dz * dz > r.rho2 * 1e-28f;
-                const double ck = voxel_anchor<EXACT>(pp2, dz64, dz, r);
-                walk_rows<true>(r, ck, pp2, fb2, dz, h, corrected, per_row_r, inv_r2_fixed, rows,
-                                emit);
+                const bool corrected = corr && r.halfw > 0.f && dz2 > r.rho2 * 1e-28f;
+                const float u = fmaf(dz, r.kc, u0);
+                const int ccol = r.n - tn0;
+                const bool col_in = tile_ok && unsigned(ccol) < unsigned(tcols);
+                const int cbase = ccol * tstride - tm0;
+                walk_rows<true>(r, m_ref, u, pm, dz, h, corrected, per_row_r, inv_r2_fixed, rows,
+                                [&](int m, int n, float vol, float inv_r2) {
+                                    const float w = vol * inv_r2;
+                                    const bool in_tile =
+                                        col_in && unsigned(m - tm0) < unsigned(trows);
+                                    if (FWD) {
+                                        if (in_tile) {
+                                            atomicAdd(&tile[cbase + m], mu * w);
+                                        } else {
+                                            const size_t px = size_t(m) * cols + n;
+                                            atomicAdd(out_img + px, mu * w * __ldg(scale + px));
+                                        }
+                                    } else {
+                                        if (in_tile) {
+                                            acc += tile[cbase + m] * w;
+                                        } else {
+                                            const size_t px = size_t(m) * cols + n;
+                                            acc += __ldg(in_img + px) * __ldg(scale + px) * w;
+                                        }
+                                    }
+                                });
             };
             if (active) {
                 const int ncached = min(cnt, MAXC);
                 for (int q = 0; q < ncached; ++q) do_cut(load_cut(s, q * NCOL + c));
             }
             if (cnt > MAXC) {
-                // rare overflow (very small pixels vs voxels): recompute cuts >= MAXC
+                // rare overflow (pixels much smaller than voxels): recompute cuts >= MAXC
                 const int i = i0 + (c % BI), j = j0 + (c / BI);
-                const ViewG<G> vgm = load_view_g<G>(vc);
-                float rc;
+                ColumnRec col;
                 int idx = 0;
-                visit_column_cuts<G>(vc, vgm, sc, i, j, true, corr, &rc, [&](const CutRec& r) {
+                column_cuts<EXACT>(vc, sc, i, j, true, corr, col, [&](const CutRec& r) {
                     if (idx++ >= MAXC && active) do_cut(r);
                 });
             }
@@ -383,16 +379,13 @@ __global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, i
                                    int corr_opt, int per_row_r, int clamp, int cap, int* rows_out,
                                    int* cols_out, double* vol_out, double* inv_out, int* n_out,
                                    int* err) {
-    using G = typename std::conditional<EXACT, double, float>::type;
     const ViewConst vc = views[view];
-    const ViewG<G> vgm = load_view_g<G>(vc);
     const double zc64 = sc.minz + (k + 0.5) * sc.a3;
     const double dz64 = zc64 - vc.s3;
     const float dz = EXACT ? float(dz64) : float(zc64) - float(vc.s3);
     const float h = float(0.5 * sc.a3);
     const bool corr = corr_opt != 0;
     int count = 0;
-    float rc;
     auto emit = [&](int m, int n, float vol, float inv_r2) {
         if (count < cap) {
             rows_out[count] = m;
@@ -402,24 +395,26 @@ __global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, i
         }
         ++count;
     };
-    // first pass only gets rho2c
-    const int st = visit_column_cuts<G>(vc, vgm, sc, i, j, clamp != 0, corr, &rc,
-                                        [&](const CutRec&) {});
+    ColumnRec col;
+    const int st = column_cuts<EXACT>(vc, sc, i, j, clamp != 0, corr, col, [&](const CutRec&) {});
     if (st < 0) {
-        *err = st == -1 ? kDevSourcePlane : kDevDegenerate;
+        *err = kDevSourcePlane;
         *n_out = 0;
         return;
     }
-    const float inv_r2_fixed = per_row_r ? -1.f : 1.f / (rc + dz * dz);
-    visit_column_cuts<G>(vc, vgm, sc, i, j, clamp != 0, corr, &rc, [&](const CutRec& r) {
+    int m_ref;
+    float u0, pm;
+    voxel_anchor<EXACT>(vc.pp2, dz64, dz, col.Q0, m_ref, u0, pm);
+    const float inv_r2_fixed = per_row_r ? -1.f : fast_rcp(col.rho2c + dz * dz);
+    column_cuts<EXACT>(vc, sc, i, j, clamp != 0, corr, col, [&](const CutRec& r) {
         const bool corrected = corr && r.halfw > 0.f && dz * dz > r.rho2 * 1e-28f;
-        const double ck = voxel_anchor<EXACT>(vc.pp2, dz64, dz, r);
+        const float u = fmaf(dz, r.kc, u0);
         if (clamp)
-            walk_rows<true>(r, ck, vc.pp2, float(vc.f_over_b2), dz, h, corrected, per_row_r != 0,
-                            inv_r2_fixed, sc.rows, emit);
+            walk_rows<true>(r, m_ref, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
+                            sc.rows, emit);
         else
-            walk_rows<false>(r, ck, vc.pp2, float(vc.f_over_b2), dz, h, corrected, per_row_r != 0,
-                             inv_r2_fixed, sc.rows, emit);
+            walk_rows<false>(r, m_ref, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
+                             sc.rows, emit);
     });
     *n_out = count;
 }
