@@ -204,6 +204,7 @@ struct cvpb_context {
     bool pixel_mismatch = false;    // (cvp.cpp:239-241)
     bool base_reaches_source = false;  // (cvp.cpp:82-84), resolved for the whole box
     int n_slots = 0;
+    int cvp_tile_need = 0;    // floats, largest brick footprint over the scene
     DevBuf<ViewConst> d_views;
     DevBuf<float> d_scale_cos, d_scale_exact;
     DevBuf<int> d_err, d_box, d_flag;
@@ -299,6 +300,7 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     L.cut_centroid = opts->r_estimate == CVPB_R_CUT_CENTROID ? 1 : 0;
     L.accumulate = accumulate;
     L.deterministic = exec ? exec->deterministic : 0;
+    L.tile_need = ctx->cvp_tile_need;
     L.err = ctx->d_err.p;
     if (!forward && view_count == 0 && !accumulate) {
         CVPB_CUDA(cudaMemsetAsync(vol_out, 0, sizeof(float) * ctx->nvox(), st));
@@ -484,6 +486,9 @@ int cvpb_set_geometry(cvpb_context* ctx, const cvpb_volume_geometry* vol,
     if (n_views > 0)  // scale slots were assigned after the first copy
         CVPB_CUDA(cudaMemcpyAsync(ctx->d_views.p, ctx->vconst.data(), sizeof(ViewConst) * n_views,
                                   cudaMemcpyHostToDevice, ctx->stream));
+    CVPB_CUDA(cvpb::launch_cvp_tile_need(sc, ctx->d_views.p, n_views, ctx->d_flag.p, ctx->stream));
+    CVPB_CUDA(cudaMemcpyAsync(&ctx->cvp_tile_need, ctx->d_flag.p, sizeof(int), cudaMemcpyDeviceToHost,
+                              ctx->stream));
     CVPB_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->has_geometry = true;
     return CVPB_OK;

@@ -133,7 +133,7 @@ __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene
 }
 
 template <bool EXACT, bool FWD>
-__global__ void __launch_bounds__(NT, 2) cvp_brick_kernel(CvpParams p) {
+__global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
     float* tile = reinterpret_cast<float*>(smem_raw + sizeof(Smem));
@@ -424,14 +424,54 @@ template <bool EXACT, bool FWD> cudaError_t setup_kernel(int dyn_smem) {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
 }
 
+// Largest tile (odd row stride x columns) any brick needs under any view.
+__global__ void tile_need_kernel(Scene sc, const ViewConst* views, int n_views, int* need) {
+    const int nbi = (sc.n1 + BI - 1) / BI, nbj = (sc.n2 + BJ - 1) / BJ, nbk = (sc.n3 + BK - 1) / BK;
+    const long long total = (long long)nbi * nbj * nbk * n_views;
+    int best = 0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        long long b = t / n_views;
+        const int v = int(t % n_views);
+        const int bi = int(b % nbi);
+        b /= nbi;
+        const int bj = int(b % nbj), bk = int(b / nbj);
+        const int i0 = bi * BI, j0 = bj * BJ, k0 = bk * BK;
+        int m0, m1, n0, n1;
+        brick_footprint(views[v], sc, i0, min(i0 + BI, sc.n1), j0, min(j0 + BJ, sc.n2), k0,
+                        min(k0 + BK, sc.n3), m0, m1, n0, n1);
+        const int tr = max(m1 - m0 + 1, 0), tc = max(n1 - n0 + 1, 0);
+        best = max(best, (tr | 1) * tc);
+    }
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(need, best);
+}
+
 }  // namespace
 
-int cvp_tile_cap_floats() { return 6144; }
+cudaError_t launch_cvp_tile_need(const Scene& sc, const ViewConst* views, int n_views, int* d_need,
+                                 cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(d_need, 0, sizeof(int), stream);
+    if (e != cudaSuccess || n_views <= 0) return e;
+    tile_need_kernel<<<148 * 4, 256, 0, stream>>>(sc, views, n_views, d_need);
+    return cudaGetLastError();
+}
+
+namespace {
+// Shared-memory budget per CTA for three resident CTAs per SM (228 KB SM
+// carve-out, 1 KB reserved per CTA) and the hard cap for the detector tile.
+constexpr int kSmemBudget3 = (228 * 1024) / 3 - 1024;
+constexpr int kTileCapMax = 16384;
+}  // namespace
 
 cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
     const Scene& sc = L.sc;
     if (L.view_count <= 0) return cudaSuccess;
-    const int tile_cap = cvp_tile_cap_floats();
+    // size the detector tile to the scene's largest brick footprint; three
+    // CTAs per SM when it fits the budget, otherwise two with a larger tile
+    int tile_cap = std::min(std::max(L.tile_need, 1), kTileCapMax);
+    const int fit3 = (kSmemBudget3 - int(sizeof(Smem))) / int(sizeof(float));
+    if (tile_cap <= fit3) tile_cap = fit3;
     const int dyn = int(sizeof(Smem)) + tile_cap * int(sizeof(float));
     const int nbricks = ((sc.n1 + BI - 1) / BI) * ((sc.n2 + BJ - 1) / BJ) * ((sc.n3 + BK - 1) / BK);
     // Enough CTAs to fill 148 SMs x 2 resident: split views into groups when

@@ -19,10 +19,12 @@ struct CvpLaunch {
     int view_begin, view_count;
     int forward, exact, elevation_correction, cut_centroid;
     int accumulate, deterministic;
+    int tile_need;            // largest brick footprint (floats), see launch_cvp_tile_need
     int* err;                 // device error flag
 };
 
-int cvp_tile_cap_floats();
+cudaError_t launch_cvp_tile_need(const Scene& sc, const ViewConst* views, int n_views, int* d_need,
+                                 cudaStream_t stream);
 cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream);
 cudaError_t launch_scale_image(double f, double pp1, double pp2, double b1, double b2, int rows,
                                int cols, int exact, float* out, double* out64, cudaStream_t stream);
