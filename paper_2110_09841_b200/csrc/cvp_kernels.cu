@@ -64,6 +64,8 @@ struct Smem {
     int nz[NCOL];             // forward: column has a nonzero voxel in the brick
     float vox[NCOL * MUS];    // forward: mu; backward: accumulators
     int tile_m0, tile_n0, tile_rows, tile_cols, tile_stride, tile_ok;
+    float mu_abs_max;         // forward: max |mu| over the brick
+    float qscale;             // forward: fixed-point scale of this (brick, view)
 };
 
 __device__ __forceinline__ void store_cut(Smem& s, int slot, const CutRec& r) {
@@ -93,7 +95,8 @@ __device__ __forceinline__ CutRec load_cut(const Smem& s, int slot) {
 // global fallback path.
 __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene& sc, int i0, int i1,
                                                 int j0, int j1, int k0, int k1, int& m0, int& m1,
-                                                int& n0, int& n1) {
+                                                int& n0, int& n1, double* depth_min = nullptr,
+                                                double* depth_max = nullptr) {
     const double xs[2] = {sc.minx + i0 * sc.a1, sc.minx + i1 * sc.a1};
     const double ys[2] = {sc.miny + j0 * sc.a2, sc.miny + j1 * sc.a2};
     double cmin = INFINITY, cmax = -INFINITY, dmin = INFINITY, dmax = -INFINITY;
@@ -107,6 +110,8 @@ __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene
             dmin = fmin(dmin, d);
             dmax = fmax(dmax, d);
         }
+    if (depth_min) *depth_min = dmin;
+    if (depth_max) *depth_max = dmax;
     const double margin = 0.5 * sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2);
     dmin -= margin;
     dmax += margin;
@@ -137,6 +142,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
     float* tile = reinterpret_cast<float*>(smem_raw + sizeof(Smem));
+    int* itile = reinterpret_cast<int*>(tile);  // forward: fixed-point accumulators
 
     const Scene& sc = p.sc;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -156,7 +162,9 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
     const size_t plane = size_t(sc.n1) * sc.n2;
     // Stage the brick's voxels: [column][k] with odd stride (bank-conflict free).
     if (tid < NCOL) s.nz[tid] = 0;
+    if (tid == 0) s.mu_abs_max = 0.f;
     __syncthreads();
+    float abs_max = 0.f;
     for (int idx = tid; idx < NCOL * BK; idx += NT) {
         const int kk = idx / NCOL, c = idx % NCOL;
         const int i = i0 + (c % BI), j = j0 + (c / BI), k = k0 + kk;
@@ -164,8 +172,14 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
         if (FWD && i < i1 && j < j1 && k < k1) {
             val = __ldg(p.vol_in + size_t(k) * plane + size_t(j) * sc.n1 + i);
             if (val != 0.f) s.nz[c] = 1;
+            abs_max = fmaxf(abs_max, fabsf(val));
         }
         s.vox[c * MUS + kk] = val;
+    }
+    if (FWD) {
+        for (int o = 16; o > 0; o >>= 1) abs_max = fmaxf(abs_max, __shfl_xor_sync(0xffffffffu, abs_max, o));
+        // non-negative floats order like their bit patterns
+        if (lane == 0) atomicMax(reinterpret_cast<int*>(&s.mu_abs_max), __float_as_int(abs_max));
     }
 
     const int rows = sc.rows, cols = sc.cols;
@@ -201,7 +215,24 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
         }
         if (tid == 0) {
             int m0, m1, n0, n1;
-            brick_footprint(vc, sc, i0, i1, j0, j1, k0, k1, m0, m1, n0, n1);
+            double dmin = 0.0, dmax = 0.0;
+            brick_footprint(vc, sc, i0, i1, j0, j1, k0, k1, m0, m1, n0, n1, &dmin, &dmax);
+            if (FWD) {
+                // Forward accumulation is int32 fixed point (native ATOMS.ADD;
+                // float shared atomics are CAS loops on sm_100). Bound on any
+                // pixel's partial sum from this brick:
+                //   |mu| <= mu_max;  inv_r2 <= 1/dmin^2 (r >= depth >= dmin);
+                //   sum of cut areas in one detector column <= area of that
+                //     column's wedge between depths dmin..dmax <= b1 dmax/f (dmax-dmin);
+                //   sum over a column stack of one row's shares <= the row's
+                //     z-window at the widest elevation depth <= b2 (dmax + diag/2)/f.
+                // Scale 2^30 / bound keeps every partial inside int32.
+                const double diag = sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2);
+                const double area = vc.b1 * dmax / vc.f * fmax(dmax - dmin, 1e-30 * dmax);
+                const double zwin = vc.b2 * (dmax + 0.5 * diag) / vc.f;
+                const double bound = double(s.mu_abs_max) * area * zwin / (dmin * dmin) * 1.05;
+                s.qscale = (bound > 0.0 && dmin > 0.0) ? float(1073741824.0 / bound) : 0.f;
+            }
             const int tr = max(m1 - m0 + 1, 0), tc = max(n1 - n0 + 1, 0);
             const int stride = tr | 1;
             s.tile_m0 = m0;
@@ -221,7 +252,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
         if (tile_ok) {
             const int ntile = trows * tcols;
             if (FWD) {
-                for (int idx = tid; idx < tstride * tcols; idx += NT) tile[idx] = 0.f;
+                for (int idx = tid; idx < tstride * tcols; idx += NT) itile[idx] = 0;
             } else {
                 const float* img = p.proj_in + vloc * npx;
                 for (int idx = tid; idx < ntile; idx += NT) {
@@ -238,6 +269,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
         const float dz = EXACT ? float(dz64) : float(zc64) - float(vc.s3);
         const float dz2 = dz * dz;
         float* out_img = FWD ? p.proj_out + vloc * npx : nullptr;
+        const float qs = FWD ? s.qscale : 0.f;
         const float* in_img = FWD ? nullptr : p.proj_in + vloc * npx;
         for (int c = warp; c < NCOL; c += NWARP) {
             const int cnt = s.count[c];
@@ -266,7 +298,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                                         col_in && unsigned(m - tm0) < unsigned(trows);
                                     if (FWD) {
                                         if (in_tile) {
-                                            atomicAdd(&tile[cbase + m], mu * w);
+                                            atomicAdd(&itile[cbase + m], __float2int_rn(mu * w * qs));
                                         } else {
                                             const size_t px = size_t(m) * cols + n;
                                             atomicAdd(out_img + px, mu * w * __ldg(scale + px));
@@ -300,12 +332,13 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
         if (FWD && tile_ok) {
             __syncthreads();
             const int ntile = trows * tcols;
+            const float inv_qs = qs > 0.f ? 1.f / qs : 0.f;
             for (int idx = tid; idx < ntile; idx += NT) {
                 const int r = idx / tcols, cc = idx % tcols;
-                const float val = tile[cc * tstride + r];
-                if (val != 0.f) {
+                const int q = itile[cc * tstride + r];
+                if (q != 0) {
                     const size_t px = size_t(tm0 + r) * cols + (tn0 + cc);
-                    atomicAdd(out_img + px, val * __ldg(scale + px));
+                    atomicAdd(out_img + px, float(q) * inv_qs * __ldg(scale + px));
                 }
             }
         }
