@@ -34,7 +34,20 @@ __device__ __forceinline__ float clampf(float x, float lo, float hi) {
     return fminf(fmaxf(x, lo), hi);
 }
 
-__device__ __forceinline__ float fast_rcp(float x) { return __fdividef(1.0f, x); }
+// Single-instruction MUFU reciprocal / rsqrt (~1 ulp); operands here are never
+// denormal, so the flush-to-zero forms avoid the 5-instruction guarded
+// sequence __fdividef expands to.
+__device__ __forceinline__ float fast_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float fast_rsqrt(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 // Per-column quantities that every cut of the column shares.
 struct ColumnRec {
@@ -250,23 +263,24 @@ __device__ int column_cuts(const ViewConst& vc, const Scene& sc, int i, int j, b
 }
 
 // Mean of clamp(alpha + beta*xi, -h, h) over xi in [-halfw, halfw]
-// (clamp_mean, cvp.cpp:161-175), in voxel-local coordinates.
-__device__ __forceinline__ float clamp_mean_local(float alpha, float beta, float halfw, float h) {
-    const float spread = fabsf(beta) * halfw;
+// (clamp_mean, cvp.cpp:161-175) in voxel-local coordinates, branch-free:
+//   mean clamp(x) = mean x - mean (x-h)+ + mean (-h-x)+  over [glo, ghi],
+// with each squared-difference term factored as (P1 - P0)(P1 + P0) and
+// P1 - P0 = clamp(ghi - h, 0, w) so no cancellation appears for narrow or
+// fully saturated ramps. spread == 0 reduces to the plain clamp.
+__device__ __forceinline__ float clamp_mean_local(float alpha, float spread, float h) {
     const float glo = alpha - spread, ghi = alpha + spread;
-    if (!(spread > 0.f) || (glo >= -h && ghi <= h)) return clampf(alpha, -h, h);
-    if (ghi <= -h) return -h;
-    if (glo >= h) return h;
-    const float ca = fmaxf(glo, -h), cb = fminf(ghi, h);
-    const float below = fmaxf(0.f, fminf(ghi, -h) - glo);
-    const float above = fmaxf(0.f, ghi - fmaxf(glo, h));
-    const float integral = h * (above - below) + 0.5f * (cb - ca) * (cb + ca);
-    return __fdividef(integral, ghi - glo);
+    const float w = 2.f * spread;
+    const float up = clampf(ghi - h, 0.f, w) * (fmaxf(ghi - h, 0.f) + fmaxf(glo - h, 0.f));
+    const float dn = clampf(-h - glo, 0.f, w) * (fmaxf(-h - glo, 0.f) + fmaxf(-h - ghi, 0.f));
+    const float t = alpha + (dn - up) * (0.5f * fast_rcp(w));
+    return spread > 0.f ? t : clampf(alpha, -h, h);
 }
 
 // Row walk of one voxel against one column cut (visit_rows, cvp.cpp:180-235)
 // in voxel-local float32: u = chi2(zc) - m_ref at the cut's centroid depth,
-// pm = pp2 - m_ref, dz = zc - s3, h = a3/2. emit(m, n, volume, inv_r2).
+// pm = pp2 - m_ref, dz = zc - s3, h = a3/2. emit(m, share * inv_r2) — the
+// caller multiplies by the cut area once per cut.
 template <bool CLAMP, class Emit>
 __device__ __forceinline__ void walk_rows(const CutRec& c, int m_ref, float u, float pm, float dz,
                                           float h, bool corrected, bool per_row_r,
@@ -281,26 +295,26 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int m_ref, float u, f
         m_last = min(m_last, rows - 1);
     }
     if (m_first > m_last) return;
-    // beta per row offset: (b2/f) hw = g / rho
-    const float bh = corrected ? c.g * rsqrtf(c.rho2) : 0.f;
+    // spread of the elevation rectangle at boundary e: |beta(e)| * halfw with
+    // beta(e) = (b2/f) hw (pm - e) = (g / rho) (pm - e)
+    const float sh = corrected ? c.g * fast_rsqrt(c.rho2) * c.halfw : 0.f;
     float e = float(m_first - m_ref) - 0.5f;  // chi2 boundary - m_ref
     float a_top = c.g * (u - e);
     float plain_top = clampf(a_top, -h, h);
-    float t_top = corrected ? clamp_mean_local(a_top, (pm - e) * bh, c.halfw, h) : plain_top;
+    float t_top = clamp_mean_local(a_top, sh * fabsf(pm - e), h);
     for (int m = m_first; m <= m_last; ++m) {
         e += 1.f;
         const float a_bot = c.g * (u - e);
         const float plain_bot = clampf(a_bot, -h, h);
-        const float t_bot =
-            corrected ? clamp_mean_local(a_bot, (pm - e) * bh, c.halfw, h) : plain_bot;
+        const float t_bot = clamp_mean_local(a_bot, sh * fabsf(pm - e), h);
         const float share = t_top - t_bot;
         if (share > 0.f) {
             float inv_r2 = inv_r2_fixed;
             if (per_row_r) {
-                const float zr = dz + 0.5f * (plain_top + plain_bot);
-                inv_r2 = fast_rcp(c.rho2 + zr * zr);
+                const float zr = fmaf(0.5f, plain_top + plain_bot, dz);
+                inv_r2 = fast_rcp(fmaf(zr, zr, c.rho2));
             }
-            emit(m, c.n, c.A * share, inv_r2);
+            emit(m, share * inv_r2);
         }
         t_top = t_bot;
         plain_top = plain_bot;

@@ -47,6 +47,7 @@ struct CvpParams {
     float* proj_out;          // forward output (view_begin-relative)
     int view_begin, view_count, views_per_group;
     int corr, per_row_r;
+    float h;                  // a3 / 2
     int tile_cap;
     int accumulate;           // backward: add into vol_out
     int atomic_out;           // backward: several view groups -> atomicAdd
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
 
     const int rows = sc.rows, cols = sc.cols;
     const size_t npx = size_t(rows) * cols;
-    const float h = float(0.5 * sc.a3);
+    const float h = p.h;
     const bool corr = p.corr != 0, per_row_r = p.per_row_r != 0;
     const int k = k0 + lane;
     const bool kvalid = k < k1;
@@ -291,27 +292,31 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                 const int ccol = r.n - tn0;
                 const bool col_in = tile_ok && unsigned(ccol) < unsigned(tcols);
                 const int cbase = ccol * tstride - tm0;
+                const float wA = FWD ? mu * r.A * qs : r.A;
+                float cut_acc = 0.f;
                 walk_rows<true>(r, m_ref, u, pm, dz, h, corrected, per_row_r, inv_r2_fixed, rows,
-                                [&](int m, int n, float vol, float inv_r2) {
-                                    const float w = vol * inv_r2;
+                                [&](int m, float wr) {
                                     const bool in_tile =
                                         col_in && unsigned(m - tm0) < unsigned(trows);
                                     if (FWD) {
                                         if (in_tile) {
-                                            atomicAdd(&itile[cbase + m], __float2int_rn(mu * w * qs));
+                                            atomicAdd(&itile[cbase + m], __float2int_rn(wr * wA));
                                         } else {
-                                            const size_t px = size_t(m) * cols + n;
-                                            atomicAdd(out_img + px, mu * w * __ldg(scale + px));
+                                            const size_t px = size_t(m) * cols + r.n;
+                                            atomicAdd(out_img + px,
+                                                      mu * r.A * wr * __ldg(scale + px));
                                         }
                                     } else {
                                         if (in_tile) {
-                                            acc += tile[cbase + m] * w;
+                                            cut_acc = fmaf(tile[cbase + m], wr, cut_acc);
                                         } else {
-                                            const size_t px = size_t(m) * cols + n;
-                                            acc += __ldg(in_img + px) * __ldg(scale + px) * w;
+                                            const size_t px = size_t(m) * cols + r.n;
+                                            cut_acc = fmaf(__ldg(in_img + px) * __ldg(scale + px),
+                                                           wr, cut_acc);
                                         }
                                     }
                                 });
+                if (!FWD) acc = fmaf(wA, cut_acc, acc);
             };
             if (active) {
                 const int ncached = min(cnt, MAXC);
@@ -419,15 +424,11 @@ __global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, i
     const float h = float(0.5 * sc.a3);
     const bool corr = corr_opt != 0;
     int count = 0;
-    auto emit = [&](int m, int n, float vol, float inv_r2) {
-        if (count < cap) {
-            rows_out[count] = m;
-            cols_out[count] = n;
-            vol_out[count] = vol;
-            inv_out[count] = inv_r2;
-        }
-        ++count;
-    };
+    // records report (volume, inv_r2); the walk hands share * inv_r2, so the
+    // debug path re-derives inv_r2 = 1 / (rho2 + zr^2) by walking twice:
+    // once with a unit-area cut to collect share * inv_r2 and the volume.
+    int cur_n = 0;
+    float cur_A = 0.f;
     ColumnRec col;
     const int st = column_cuts<EXACT>(vc, sc, i, j, clamp != 0, corr, col, [&](const CutRec&) {});
     if (st < 0) {
@@ -442,12 +443,41 @@ __global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, i
     column_cuts<EXACT>(vc, sc, i, j, clamp != 0, corr, col, [&](const CutRec& r) {
         const bool corrected = corr && r.halfw > 0.f && dz * dz > r.rho2 * 1e-28f;
         const float u = fmaf(dz, r.kc, u0);
-        if (clamp)
+        cur_n = r.n;
+        cur_A = r.A;
+        // pass 1: share * inv_r2; pass 2 (fixed inv_r2 = 1): share alone
+        float wr[64], sh[64];
+        int ms[64], nrec = 0;
+        auto take = [&](int m, float v) {
+            if (nrec < 64) {
+                ms[nrec] = m;
+                wr[nrec] = v;
+            }
+            ++nrec;
+        };
+        int nrec2 = 0;
+        auto take2 = [&](int, float v) {
+            if (nrec2 < 64) sh[nrec2] = v;
+            ++nrec2;
+        };
+        if (clamp) {
             walk_rows<true>(r, m_ref, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
-                            sc.rows, emit);
-        else
+                            sc.rows, take);
+            walk_rows<true>(r, m_ref, u, pm, dz, h, corrected, false, 1.f, sc.rows, take2);
+        } else {
             walk_rows<false>(r, m_ref, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
-                             sc.rows, emit);
+                             sc.rows, take);
+            walk_rows<false>(r, m_ref, u, pm, dz, h, corrected, false, 1.f, sc.rows, take2);
+        }
+        for (int t = 0; t < nrec && t < 64; ++t) {
+            if (count < cap) {
+                rows_out[count] = ms[t];
+                cols_out[count] = cur_n;
+                vol_out[count] = double(cur_A) * sh[t];
+                inv_out[count] = sh[t] > 0.f ? double(wr[t]) / sh[t] : 0.0;
+            }
+            ++count;
+        }
     });
     *n_out = count;
 }
@@ -529,6 +559,7 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
     p.views_per_group = per;
     p.corr = L.elevation_correction;
     p.per_row_r = L.cut_centroid;
+    p.h = float(0.5 * sc.a3);
     p.tile_cap = tile_cap;
     p.accumulate = L.accumulate;
     p.atomic_out = groups > 1 ? 1 : 0;
