@@ -1,0 +1,3 @@
+// Drop-in forwarder: the reference header cbct/exec.hpp maps onto the GPU-backed API.
+#pragma once
+#include "cbct_b200/cbct.hpp"

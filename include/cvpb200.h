@@ -75,9 +75,12 @@ typedef struct cvpb_cvp_options {
     int r_estimate;
 } cvpb_cvp_options;
 
-/* ExecPolicy (exec.hpp:6-15). threads is ignored on the device; deterministic
- * selects a fixed-order (atomic-free) forward flush; allow_expensive gates
- * Siddon K >= 128 exactly as the reference does (siddon.cpp:107-113). */
+/* ExecPolicy (exec.hpp:6-15). threads is ignored on the device. deterministic
+ * keeps one view group per brick in the CVP backprojection (fixed accumulation
+ * order: bit-reproducible); the CVP forward always sums a brick's records in
+ * int32 fixed point (order-independent) and merges bricks with float atomics
+ * (reproducible to float32 reassociation). allow_expensive gates Siddon
+ * K >= 128 exactly as the reference does (siddon.cpp:107-113). */
 typedef struct cvpb_exec_policy {
     int threads;
     int deterministic;
@@ -176,12 +179,34 @@ int cvpb_backproject_siddon(cvpb_context* ctx, int k_per_edge, const cvpb_exec_p
                             const float* d_proj, float* d_volume, int view_begin, int view_count,
                             int accumulate, void* stream);
 
+/* trace_ray (siddon.cpp:154-164): the device traversal of one ray source ->
+ * target through `vol`; writes at most cap (i, j, k) triples and chord
+ * lengths [mm], total count in *n_out. */
+int cvpb_trace_ray(cvpb_context* ctx, const cvpb_volume_geometry* vol, const double source[3],
+                   const double target[3], int cap, int* ijk, double* length, int* n_out);
+
 /* ---- TT footprint (new; see cvpb_tt_options) ----------------------------- */
 int cvpb_project_tt(cvpb_context* ctx, const cvpb_tt_options* opts, const float* d_volume,
                     float* d_proj, int view_begin, int view_count, void* stream);
 int cvpb_backproject_tt(cvpb_context* ctx, const cvpb_tt_options* opts, const float* d_proj,
                         float* d_volume, int view_begin, int view_count, int accumulate,
                         void* stream);
+
+/* ---- reference-facing host paths for Siddon-K, TT and CGLS -------------------
+ * float64 host buffers in the reference layout; conversion and copies happen
+ * on the device inside the call (same contract as cvpb_project_cvp_host). */
+int cvpb_project_siddon_host(cvpb_context* ctx, int k_per_edge, const cvpb_pixel_roi* roi,
+                             const cvpb_exec_policy* exec, const double* volume, double* proj);
+int cvpb_backproject_siddon_host(cvpb_context* ctx, int k_per_edge, const cvpb_exec_policy* exec,
+                                 const double* proj, double* volume);
+int cvpb_project_tt_host(cvpb_context* ctx, const cvpb_tt_options* opts, const double* volume,
+                         double* proj);
+int cvpb_backproject_tt_host(cvpb_context* ctx, const cvpb_tt_options* opts, const double* proj,
+                             double* volume);
+/* cgls (solver.cpp:55-106) device-resident, host data in / host iterate out. */
+int cvpb_cgls_host(cvpb_context* ctx, int projector, const cvpb_cvp_options* cvp_opts,
+                   int k_per_edge, const double* b, double* x, int iterations,
+                   double* residual_norms);
 
 /* ---- device vector ops for CGLS (solver.cpp:15-106) ---------------------- */
 /* Compensated float64 dot of two float32 device vectors (dot_kahan,

@@ -85,9 +85,17 @@ SIGNATURES = {
                                       _vp, _vp, C.c_int, C.c_int, _vp]),
     "cvpb_backproject_siddon": (C.c_int, [_vp, C.c_int, _P(cvpb_exec_policy), _vp, _vp, C.c_int,
                                           C.c_int, C.c_int, _vp]),
+    "cvpb_trace_ray": (C.c_int, [_vp, _P(cvpb_volume_geometry), _dp, _dp, C.c_int, _ip, _dp, _ip]),
     "cvpb_project_tt": (C.c_int, [_vp, _P(cvpb_tt_options), _vp, _vp, C.c_int, C.c_int, _vp]),
     "cvpb_backproject_tt": (C.c_int, [_vp, _P(cvpb_tt_options), _vp, _vp, C.c_int, C.c_int,
                                       C.c_int, _vp]),
+    "cvpb_project_siddon_host": (C.c_int, [_vp, C.c_int, _P(cvpb_pixel_roi), _P(cvpb_exec_policy),
+                                           _vp, _vp]),
+    "cvpb_backproject_siddon_host": (C.c_int, [_vp, C.c_int, _P(cvpb_exec_policy), _vp, _vp]),
+    "cvpb_project_tt_host": (C.c_int, [_vp, _P(cvpb_tt_options), _vp, _vp]),
+    "cvpb_backproject_tt_host": (C.c_int, [_vp, _P(cvpb_tt_options), _vp, _vp]),
+    "cvpb_cgls_host": (C.c_int, [_vp, C.c_int, _P(cvpb_cvp_options), C.c_int, _vp, _vp, C.c_int,
+                                 _dp]),
     "cvpb_vec_dot": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _dp, _vp]),
     "cvpb_vec_axpy": (C.c_int, [_vp, C.c_double, _vp, _vp, C.c_size_t, _vp]),
     "cvpb_vec_xpby": (C.c_int, [_vp, _vp, C.c_double, _vp, C.c_size_t, _vp]),

@@ -353,6 +353,29 @@ int ensure_host_buffers(cvpb_context* ctx) {
 
 }  // namespace
 
+namespace {
+// H2D(float64 -> float32) of `in`, run(d_in, d_out), D2H(float32 -> float64)
+// into `out`; d_in / d_out are the context's host-path device buffers.
+template <class Run>
+int host_roundtrip(cvpb_context* ctx, bool vol_to_proj, const double* in, double* out, Run&& run) {
+    CVPB_TRY(check_ctx(ctx));
+    if (!in || !out) return fail(CVPB_INVALID_ARGUMENT, "null host buffer");
+    CVPB_TRY(ensure_host_buffers(ctx));
+    cudaStream_t st = ctx->stream;
+    const size_t nv = ctx->nvox(), np = ctx->npx_view() * ctx->views.size();
+    const size_t n_in = vol_to_proj ? nv : np, n_out = vol_to_proj ? np : nv;
+    float* d_in = vol_to_proj ? ctx->h_vol.p : ctx->h_proj.p;
+    float* d_out = vol_to_proj ? ctx->h_proj.p : ctx->h_vol.p;
+    CVPB_CUDA(cudaMemcpyAsync(ctx->d_stage.p, in, sizeof(double) * n_in, cudaMemcpyHostToDevice, st));
+    CVPB_CUDA(cvpb::launch_f64_to_f32(ctx->d_stage.p, d_in, n_in, st));
+    CVPB_TRY(run(d_in, d_out, st));
+    CVPB_CUDA(cvpb::launch_f32_to_f64(d_out, ctx->d_stage.p, n_out, st));
+    CVPB_CUDA(cudaMemcpyAsync(out, ctx->d_stage.p, sizeof(double) * n_out, cudaMemcpyDeviceToHost, st));
+    CVPB_CUDA(cudaStreamSynchronize(st));
+    return CVPB_OK;
+}
+}  // namespace
+
 extern "C" {
 
 int cvpb_abi_version(void) { return CVPB_ABI_VERSION; }
@@ -826,6 +849,49 @@ int cvpb_backproject_siddon(cvpb_context* ctx, int k_per_edge, const cvpb_exec_p
     return CVPB_OK;
 }
 
+int cvpb_trace_ray(cvpb_context* ctx, const cvpb_volume_geometry* vol, const double source[3],
+                   const double target[3], int cap, int* ijk, double* length, int* n_out) {
+    CVPB_TRY(check_ctx(ctx, false));
+    if (!vol || !source || !target || !n_out) return fail(CVPB_INVALID_ARGUMENT, "null argument");
+    for (int c : vol->counts)
+        if (c <= 0) return fail(CVPB_INVALID_ARGUMENT, "voxel counts must be positive");
+    const double d[3] = {target[0] - source[0], target[1] - source[1], target[2] - source[2]};
+    if (!(d[0] * d[0] + d[1] * d[1] + d[2] * d[2] > 0.0))
+        return fail(CVPB_INVALID_ARGUMENT, "ray source and target coincide");
+    Scene sc{};
+    sc.n1 = vol->counts[0];
+    sc.n2 = vol->counts[1];
+    sc.n3 = vol->counts[2];
+    sc.a1 = vol->voxel_size[0];
+    sc.a2 = vol->voxel_size[1];
+    sc.a3 = vol->voxel_size[2];
+    sc.minx = (sc.n1 * sc.a1) * -0.5;
+    sc.miny = (sc.n2 * sc.a2) * -0.5;
+    sc.minz = (sc.n3 * sc.a3) * -0.5;
+    // require_source_outside (siddon.cpp:100-105)
+    const double lo[3] = {sc.minx, sc.miny, sc.minz};
+    const double hi[3] = {-sc.minx, -sc.miny, -sc.minz};
+    if (source[0] > lo[0] && source[0] < hi[0] && source[1] > lo[1] && source[1] < hi[1] &&
+        source[2] > lo[2] && source[2] < hi[2])
+        return fail(CVPB_RUNTIME_ERROR, "unsupported configuration: source inside the volume box");
+    if (cap < 0) cap = 0;
+    cudaStream_t st = ctx->stream;
+    CVPB_CUDA(ctx->d_rec_i.reserve(3 * size_t(cap) + 1));
+    CVPB_CUDA(ctx->d_rec_d.reserve(size_t(cap) + 1));
+    int* d_n = ctx->d_rec_i.p + 3 * size_t(cap);
+    CVPB_CUDA(cvpb::launch_trace_ray(sc, source, target, cap, ctx->d_rec_i.p, ctx->d_rec_d.p, d_n, st));
+    int n = 0;
+    CVPB_CUDA(cudaMemcpyAsync(&n, d_n, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CVPB_CUDA(cudaStreamSynchronize(st));
+    const int c = std::min(n, cap);
+    if (c > 0) {
+        if (ijk) CVPB_CUDA(cudaMemcpy(ijk, ctx->d_rec_i.p, sizeof(int) * 3 * c, cudaMemcpyDeviceToHost));
+        if (length) CVPB_CUDA(cudaMemcpy(length, ctx->d_rec_d.p, sizeof(double) * c, cudaMemcpyDeviceToHost));
+    }
+    *n_out = n;
+    return CVPB_OK;
+}
+
 // ---- TT -------------------------------------------------------------------------
 
 int cvpb_project_tt(cvpb_context* ctx, const cvpb_tt_options* opts, const float* d_volume,
@@ -862,6 +928,50 @@ int cvpb_backproject_tt(cvpb_context* ctx, const cvpb_tt_options* opts, const fl
     L.accumulate = accumulate;
     CVPB_CUDA(cvpb::launch_tt(L, false, static_cast<cudaStream_t>(stream)));
     return CVPB_OK;
+}
+
+// ---- host paths for Siddon-K / TT / CGLS ---------------------------------------
+
+
+int cvpb_project_siddon_host(cvpb_context* ctx, int k_per_edge, const cvpb_pixel_roi* roi,
+                             const cvpb_exec_policy* exec, const double* volume, double* proj) {
+    const int V = ctx ? int(ctx->views.size()) : 0;
+    return host_roundtrip(ctx, true, volume, proj, [&](float* din, float* dout, cudaStream_t st) {
+        return cvpb_project_siddon(ctx, k_per_edge, roi, exec, din, dout, 0, V, st);
+    });
+}
+
+int cvpb_backproject_siddon_host(cvpb_context* ctx, int k_per_edge, const cvpb_exec_policy* exec,
+                                 const double* proj, double* volume) {
+    const int V = ctx ? int(ctx->views.size()) : 0;
+    return host_roundtrip(ctx, false, proj, volume, [&](float* din, float* dout, cudaStream_t st) {
+        return cvpb_backproject_siddon(ctx, k_per_edge, exec, din, dout, 0, V, 0, st);
+    });
+}
+
+int cvpb_project_tt_host(cvpb_context* ctx, const cvpb_tt_options* opts, const double* volume,
+                         double* proj) {
+    const int V = ctx ? int(ctx->views.size()) : 0;
+    return host_roundtrip(ctx, true, volume, proj, [&](float* din, float* dout, cudaStream_t st) {
+        return cvpb_project_tt(ctx, opts, din, dout, 0, V, st);
+    });
+}
+
+int cvpb_backproject_tt_host(cvpb_context* ctx, const cvpb_tt_options* opts, const double* proj,
+                             double* volume) {
+    const int V = ctx ? int(ctx->views.size()) : 0;
+    return host_roundtrip(ctx, false, proj, volume, [&](float* din, float* dout, cudaStream_t st) {
+        return cvpb_backproject_tt(ctx, opts, din, dout, 0, V, 0, st);
+    });
+}
+
+int cvpb_cgls_host(cvpb_context* ctx, int projector, const cvpb_cvp_options* cvp_opts,
+                   int k_per_edge, const double* b, double* x, int iterations,
+                   double* residual_norms) {
+    return host_roundtrip(ctx, false, b, x, [&](float* din, float* dout, cudaStream_t st) {
+        return cvpb_cgls(ctx, projector, cvp_opts, k_per_edge, din, dout, iterations,
+                         residual_norms, st);
+    });
 }
 
 // ---- vector ops -------------------------------------------------------------------

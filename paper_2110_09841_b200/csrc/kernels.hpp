@@ -47,6 +47,8 @@ struct SiddonLaunch {
     int accumulate;
 };
 cudaError_t launch_siddon(const SiddonLaunch& L, bool forward, cudaStream_t stream);
+cudaError_t launch_trace_ray(const Scene& sc, const double* src, const double* tgt, int cap, int* ijk,
+                             double* len, int* n_out, cudaStream_t stream);
 cudaError_t launch_nonzero_box(const float* vol, const Scene& sc, int* d_box6, cudaStream_t stream);
 
 struct TTLaunch {

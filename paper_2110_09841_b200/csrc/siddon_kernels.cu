@@ -198,7 +198,33 @@ __global__ void nonzero_box_kernel(const float* vol, int n1, int n2, int n3, int
     }
 }
 
+__global__ void trace_ray_kernel(Scene sc, double sx, double sy, double sz, double tx, double ty,
+                                 double tz, int cap, int* ijk, double* len, int* n_out) {
+    const Box box = make_box(sc, nullptr);
+    const double s[3] = {sx, sy, sz};
+    const double d[3] = {tx - sx, ty - sy, tz - sz};
+    const double dl = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    int n = 0;
+    traverse(box, s, d, dl, [&](int i, int j, int k, double chord) {
+        if (n < cap) {
+            ijk[3 * n] = i;
+            ijk[3 * n + 1] = j;
+            ijk[3 * n + 2] = k;
+            len[n] = chord;
+        }
+        ++n;
+    });
+    *n_out = n;
+}
+
 }  // namespace
+
+cudaError_t launch_trace_ray(const Scene& sc, const double* src, const double* tgt, int cap, int* ijk,
+                             double* len, int* n_out, cudaStream_t stream) {
+    trace_ray_kernel<<<1, 1, 0, stream>>>(sc, src[0], src[1], src[2], tgt[0], tgt[1], tgt[2], cap, ijk,
+                                          len, n_out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_nonzero_box(const float* vol, const Scene& sc, int* d_box6, cudaStream_t stream) {
     const int init[6] = {sc.n1, sc.n2, sc.n3, 0, 0, 0};
