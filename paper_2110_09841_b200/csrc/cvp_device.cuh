@@ -263,18 +263,19 @@ __device__ int column_cuts(const ViewConst& vc, const Scene& sc, int i, int j, b
 }
 
 // Mean of clamp(alpha + beta*xi, -h, h) over xi in [-halfw, halfw]
-// (clamp_mean, cvp.cpp:161-175) in voxel-local coordinates, branch-free:
-//   mean clamp(x) = mean x - mean (x-h)+ + mean (-h-x)+  over [glo, ghi],
-// with each squared-difference term factored as (P1 - P0)(P1 + P0) and
-// P1 - P0 = clamp(ghi - h, 0, w) so no cancellation appears for narrow or
-// fully saturated ramps. spread == 0 reduces to the plain clamp.
+// (clamp_mean, cvp.cpp:161-175) in voxel-local coordinates, branch-free.
+// With spread s = |beta| halfw, mean over [alpha-s, alpha+s] of
+//   min(u, h)  = min(alpha, h)  - (s - |alpha - h|)+^2 / (4s)
+//   max(u, -h) = max(alpha, -h) + (s - |alpha + h|)+^2 / (4s)
+// and clamp = min + max - u, so
+//   T = clamp(alpha, -h, h) + [(s - |alpha+h|)+^2 - (s - |alpha-h|)+^2] / (4s),
+// exact for any s (also ramps wider than the voxel); both squares are <= s^2,
+// so the correction stays bounded as s -> 0 and vanishes at s = 0.
 __device__ __forceinline__ float clamp_mean_local(float alpha, float spread, float h) {
-    const float glo = alpha - spread, ghi = alpha + spread;
-    const float w = 2.f * spread;
-    const float up = clampf(ghi - h, 0.f, w) * (fmaxf(ghi - h, 0.f) + fmaxf(glo - h, 0.f));
-    const float dn = clampf(-h - glo, 0.f, w) * (fmaxf(-h - glo, 0.f) + fmaxf(-h - ghi, 0.f));
-    const float t = alpha + (dn - up) * (0.5f * fast_rcp(w));
-    return spread > 0.f ? t : clampf(alpha, -h, h);
+    const float d1 = fmaxf(spread - fabsf(alpha + h), 0.f);
+    const float d2 = fmaxf(spread - fabsf(alpha - h), 0.f);
+    const float corr = fmaf(d1, d1, -d2 * d2) * (0.25f * fast_rcp(fmaxf(spread, 1e-30f)));
+    return clampf(alpha, -h, h) + corr;
 }
 
 // Row walk of one voxel against one column cut (visit_rows, cvp.cpp:180-235)
