@@ -303,6 +303,9 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int m_ref, float u, f
     float a_top = c.g * (u - e);
     float plain_top = clampf(a_top, -h, h);
     float t_top = clamp_mean_local(a_top, sh * fabsf(pm - e), h);
+    // not unrolled: rows per voxel-cut are 1-3 and differ across lanes; an
+    // unrolled pair + remainder runs the remainder with ~2 active lanes
+#pragma unroll 1
     for (int m = m_first; m <= m_last; ++m) {
         e += 1.f;
         const float a_bot = c.g * (u - e);

@@ -21,6 +21,7 @@
 // The brick's attenuation values (forward) / accumulators (backward) stay in
 // shared memory across all views, so HBM sees the volume once per launch.
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 
 #include "cvp_device.cuh"
@@ -69,13 +70,49 @@ struct Smem {
     float qscale;             // forward: fixed-point scale of this (brick, view)
 };
 
+// 32-bit shared-window addressing for the hot paths: with 80 registers the
+// compiler otherwise rematerialises the generic->shared window base
+// (S2R SR_CgaCtaId + LEA) at every access.
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float4 lds_f32x4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void red_s32(uint32_t a, int v) {
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void store_cut(Smem& s, int slot, const CutRec& r) {
     s.cutA[slot] = make_float4(r.A, r.g, r.rho2, r.halfw);
     s.cutB[slot] = make_float4(r.kc, r.tr_a, r.tr_b, __int_as_float(r.n));
 }
 
-__device__ __forceinline__ CutRec load_cut(const Smem& s, int slot) {
-    const float4 a = s.cutA[slot], b = s.cutB[slot];
+__device__ __forceinline__ CutRec load_cut(uint32_t sbase, int slot) {
+    const float4 a = lds_f32x4(sbase + uint32_t(offsetof(Smem, cutA)) + 16u * slot);
+    const float4 b = lds_f32x4(sbase + uint32_t(offsetof(Smem, cutB)) + 16u * slot);
     CutRec r;
     r.A = a.x;
     r.g = a.y;
@@ -144,6 +181,8 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
     float* tile = reinterpret_cast<float*>(smem_raw + sizeof(Smem));
     int* itile = reinterpret_cast<int*>(tile);  // forward: fixed-point accumulators
+    const uint32_t sbase = saddr(smem_raw);
+    const uint32_t tbase = sbase + uint32_t(sizeof(Smem));  // detector tile
 
     const Scene& sc = p.sc;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -273,25 +312,28 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
         const float qs = FWD ? s.qscale : 0.f;
         const float* in_img = FWD ? nullptr : p.proj_in + vloc * npx;
         for (int c = warp; c < NCOL; c += NWARP) {
-            const int cnt = s.count[c];
+            const int cnt = lds_s32(sbase + uint32_t(offsetof(Smem, count)) + 4u * c);
             if (cnt == 0) continue;
+            const uint32_t vaddr = sbase + uint32_t(offsetof(Smem, vox)) + 4u * (c * MUS + lane);
             float mu = 0.f;
             if (FWD) {
-                mu = s.vox[c * MUS + lane];
+                mu = lds_f32(vaddr);
                 if (!__any_sync(0xffffffffu, kvalid && mu != 0.f)) continue;
             }
             const bool active = kvalid && (!FWD || mu != 0.f);
             int m_ref;
             float u0, pm;
-            voxel_anchor<EXACT>(pp2, dz64, dz, s.Q0[c], m_ref, u0, pm);
-            const float inv_r2_fixed = per_row_r ? -1.f : fast_rcp(s.rho2c[c] + dz2);
+            voxel_anchor<EXACT>(pp2, dz64, dz, lds_f64(sbase + uint32_t(offsetof(Smem, Q0)) + 8u * c),
+                                m_ref, u0, pm);
+            const float inv_r2_fixed =
+                per_row_r ? -1.f : fast_rcp(lds_f32(sbase + uint32_t(offsetof(Smem, rho2c)) + 4u * c) + dz2);
             float acc = 0.f;
             auto do_cut = [&](const CutRec& r) {
                 const bool corrected = corr && r.halfw > 0.f && dz2 > r.rho2 * 1e-28f;
                 const float u = fmaf(dz, r.kc, u0);
                 const int ccol = r.n - tn0;
                 const bool col_in = tile_ok && unsigned(ccol) < unsigned(tcols);
-                const int cbase = ccol * tstride - tm0;
+                const uint32_t cbase = tbase + 4u * uint32_t(ccol * tstride - tm0);
                 const float wA = FWD ? mu * r.A * qs : r.A;
                 float cut_acc = 0.f;
                 walk_rows<true>(r, m_ref, u, pm, dz, h, corrected, per_row_r, inv_r2_fixed, rows,
@@ -300,7 +342,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                                         col_in && unsigned(m - tm0) < unsigned(trows);
                                     if (FWD) {
                                         if (in_tile) {
-                                            atomicAdd(&itile[cbase + m], __float2int_rn(wr * wA));
+                                            red_s32(cbase + 4u * m, __float2int_rn(wr * wA));
                                         } else {
                                             const size_t px = size_t(m) * cols + r.n;
                                             atomicAdd(out_img + px,
@@ -308,7 +350,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                                         }
                                     } else {
                                         if (in_tile) {
-                                            cut_acc = fmaf(tile[cbase + m], wr, cut_acc);
+                                            cut_acc = fmaf(lds_f32(cbase + 4u * m), wr, cut_acc);
                                         } else {
                                             const size_t px = size_t(m) * cols + r.n;
                                             cut_acc = fmaf(__ldg(in_img + px) * __ldg(scale + px),
@@ -320,7 +362,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
             };
             if (active) {
                 const int ncached = min(cnt, MAXC);
-                for (int q = 0; q < ncached; ++q) do_cut(load_cut(s, q * NCOL + c));
+                for (int q = 0; q < ncached; ++q) do_cut(load_cut(sbase, q * NCOL + c));
             }
             if (cnt > MAXC) {
                 // rare overflow (pixels much smaller than voxels): recompute cuts >= MAXC
@@ -331,7 +373,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                     if (idx++ >= MAXC && active) do_cut(r);
                 });
             }
-            if (!FWD && kvalid) s.vox[c * MUS + lane] += acc;
+            if (!FWD && kvalid) sts_f32(vaddr, lds_f32(vaddr) + acc);
         }
         // ---- flush (forward) ----------------------------------------------
         if (FWD && tile_ok) {
