@@ -13,6 +13,7 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <random>
@@ -205,6 +206,7 @@ struct cvpb_context {
     bool base_reaches_source = false;  // (cvp.cpp:82-84), resolved for the whole box
     int n_slots = 0;
     int cvp_tile_need = 0;    // floats, largest brick footprint over the scene
+    double r_min = 0.0;       // smallest source-to-volume-box distance over the views
     DevBuf<ViewConst> d_views;
     DevBuf<float> d_scale_cos, d_scale_exact;
     DevBuf<int> d_err, d_box, d_flag;
@@ -491,6 +493,12 @@ int cvpb_set_geometry(cvpb_context* ctx, const cvpb_volume_geometry* vol,
         if (s[0] > lo[0] && s[0] < hi[0] && s[1] > lo[1] && s[1] < hi[1] && s[2] > lo[2] &&
             s[2] < hi[2])
             ctx->source_inside = true;
+        double d2 = 0.0;  // squared distance from the source to the box
+        for (int q = 0; q < 3; ++q) {
+            const double t = std::max(lo[q] - s[q], std::max(0.0, s[q] - hi[q]));
+            d2 += t * t;
+        }
+        ctx->r_min = v == 0 ? std::sqrt(d2) : std::min(ctx->r_min, std::sqrt(d2));
         // every voxel-base corner is a convex combination of the box's base
         // corners and depth is affine, so checking the 4 box corners decides
         // the reference's per-voxel depth test (cvp.cpp:82-84) for all voxels

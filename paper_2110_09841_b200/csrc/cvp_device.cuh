@@ -284,7 +284,7 @@ __device__ __forceinline__ float clamp_mean_local(float alpha, float spread, flo
 // caller multiplies by the cut area once per cut.
 template <bool CLAMP, class Emit>
 __device__ __forceinline__ void walk_rows(const CutRec& c, int m_ref, float u, float pm, float dz,
-                                          float h, bool corrected, bool per_row_r,
+                                          float h, bool corrected, const bool per_row_r,
                                           float inv_r2_fixed, int rows, Emit&& emit) {
     // rows whose boundaries can intersect the (elevation-widened) voxel
     // (cvp.cpp:183-201): symmetric bound of the four corner chi2 values

@@ -175,7 +175,9 @@ __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene
     m1 = min(int(floor(rmax + 0.5)) + 1, sc.rows - 1);
 }
 
-template <bool EXACT, bool FWD>
+// CORR: elevation correction option; CCR: CutCentroid radius estimate
+// (cvp.hpp:17-22) — compile-time so the unused paths cost no registers.
+template <bool EXACT, bool FWD, bool CORR, bool CCR>
 __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
     const int rows = sc.rows, cols = sc.cols;
     const size_t npx = size_t(rows) * cols;
     const float h = p.h;
-    const bool corr = p.corr != 0, per_row_r = p.per_row_r != 0;
+    constexpr bool corr = CORR, per_row_r = CCR;
     const int k = k0 + lane;
     const bool kvalid = k < k1;
     const double zc64 = sc.minz + (k + 0.5) * sc.a3;
@@ -524,9 +526,22 @@ __global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, i
     *n_out = count;
 }
 
-template <bool EXACT, bool FWD> cudaError_t setup_kernel(int dyn_smem) {
-    return cudaFuncSetAttribute(cvp_brick_kernel<EXACT, FWD>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
+template <bool EXACT, bool FWD, bool CORR, bool CCR>
+cudaError_t launch_variant(const CvpParams& p, dim3 grid, int dyn, cudaStream_t stream) {
+    cudaError_t e = cudaFuncSetAttribute(cvp_brick_kernel<EXACT, FWD, CORR, CCR>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    if (e != cudaSuccess) return e;
+    cvp_brick_kernel<EXACT, FWD, CORR, CCR><<<grid, NT, dyn, stream>>>(p);
+    return cudaGetLastError();
+}
+
+template <bool EXACT, bool FWD>
+cudaError_t launch_opts(const CvpParams& p, dim3 grid, int dyn, cudaStream_t stream) {
+    if (p.corr)
+        return p.per_row_r ? launch_variant<EXACT, FWD, true, true>(p, grid, dyn, stream)
+                           : launch_variant<EXACT, FWD, true, false>(p, grid, dyn, stream);
+    return p.per_row_r ? launch_variant<EXACT, FWD, false, true>(p, grid, dyn, stream)
+                       : launch_variant<EXACT, FWD, false, false>(p, grid, dyn, stream);
 }
 
 // Largest tile (odd row stride x columns) any brick needs under any view.
@@ -617,23 +632,11 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
         e = cudaMemsetAsync(L.proj_out, 0, sizeof(float) * size_t(sc.rows) * sc.cols * L.view_count,
                             stream);
         if (e != cudaSuccess) return e;
-        if (L.exact) {
-            if ((e = setup_kernel<true, true>(dyn)) != cudaSuccess) return e;
-            cvp_brick_kernel<true, true><<<grid, NT, dyn, stream>>>(p);
-        } else {
-            if ((e = setup_kernel<false, true>(dyn)) != cudaSuccess) return e;
-            cvp_brick_kernel<false, true><<<grid, NT, dyn, stream>>>(p);
-        }
-    } else {
-        if (L.exact) {
-            if ((e = setup_kernel<true, false>(dyn)) != cudaSuccess) return e;
-            cvp_brick_kernel<true, false><<<grid, NT, dyn, stream>>>(p);
-        } else {
-            if ((e = setup_kernel<false, false>(dyn)) != cudaSuccess) return e;
-            cvp_brick_kernel<false, false><<<grid, NT, dyn, stream>>>(p);
-        }
+        return L.exact ? launch_opts<true, true>(p, grid, dyn, stream)
+                       : launch_opts<false, true>(p, grid, dyn, stream);
     }
-    return cudaGetLastError();
+    return L.exact ? launch_opts<true, false>(p, grid, dyn, stream)
+                   : launch_opts<false, false>(p, grid, dyn, stream);
 }
 
 cudaError_t launch_scale_image(double f, double pp1, double pp2, double b1, double b2, int rows,
