@@ -168,6 +168,8 @@ def main():
     ap.add_argument("--ref-views", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cgls-iters", type=int, default=2,
+                    help="device-resident CGLS iterations timed for cgls_ms_per_iter (0 = skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -278,6 +280,25 @@ def main():
                        "buffers, conversions and copies inside the timed region)",
                "steps": e2e_steps}
 
+    # ---- CGLS ms/iter (BASELINE metric, second half) ---------------------------
+    cgls = None
+    if args.cgls_iters > 0 and world == 1:
+        bt = scene.project_cvp(x, opts=opts)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, res0 = scene.cgls(bt, 1, opts=opts)          # 1 BP + 1 iteration
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        _, res = scene.cgls(bt, 1 + args.cgls_iters, opts=opts)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        cgls = {"ms_per_iter": ((t2 - t1) - (t1 - t0)) / args.cgls_iters * 1e3,
+                "iterations_timed": args.cgls_iters,
+                "residual_ratio": res[-1] / res[0],
+                "how": "device-resident cvpb_cgls on the c3 scene (1 P + 1 BP + float64-accumulated "
+                       "vector ops per iteration); ms/iter = (T(1+n) - T(1)) / n, wall clock "
+                       "around synchronized calls"}
+
     # ---- roofline of the dominant kernel -----------------------------------
     hbm, peak_src = _peaks()
     dom_ms = max(pm, bm)
@@ -310,7 +331,7 @@ def main():
                           "detector": [c["rows"], c["cols"]],
                           "parallelism": f"view-sharded x{world}",
                           "l2": "inputs larger than L2 (512 MiB volume, 587 MB stack)"},
-               "p_ms": pm, "bp_ms": bm, "reduce_scatter_ms": rm if world > 1 else 0.0,
+               "p_ms": pm, "bp_ms": bm, "cgls": cgls, "reduce_scatter_ms": rm if world > 1 else 0.0,
                "p_gvps": work / (pm * 1e-3) if world == 1 else None,
                "bp_gvps": work / (bm * 1e-3) if world == 1 else None,
                "gpu_launches": 2 * args.steps,
