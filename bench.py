@@ -279,6 +279,42 @@ def main():
                "path": "cvpb_project_cvp_host + cvpb_backproject_cvp_host (float64 pinned host "
                        "buffers, conversions and copies inside the timed region)",
                "steps": e2e_steps}
+    elif not args.no_e2e:
+        # N > 1: each rank moves its own inputs (float64 pinned host: the full
+        # volume for P, its view shard for BP) and its outputs (its projection
+        # shard, its z-slab of the reduce-scattered volume) through the public
+        # API (DeviceScene + reduce-scatter); max over ranks of the wall time.
+        npx = det.pixel_count()
+        x64 = torch.from_numpy(cb.fill_uniform01(nvox, 7)).pin_memory()
+        b64 = torch.from_numpy(cb.fill_uniform01(npx * V, 8)[v0 * npx:v1 * npx].copy()).pin_memory()
+        p64 = torch.empty((v1 - v0) * npx, dtype=torch.float64).pin_memory()
+        s64 = torch.empty(slab.numel(), dtype=torch.float64).pin_memory()
+        e2e_steps = max(1, min(args.steps, 3))
+
+        def e2e_step():
+            xd = x64.to("cuda", non_blocking=True).float().reshape(geom.shape())
+            bd = b64.to("cuda", non_blocking=True).float().reshape(v1 - v0, det.rows, det.cols)
+            scene.project_cvp(xd, p, opts, view_begin=v0, view_count=v1 - v0)
+            scene.backproject_cvp(bd, bp, opts, view_begin=v0, view_count=v1 - v0)
+            dist.reduce_scatter_tensor(slab, bp.view(-1))
+            p64.copy_(p.view(-1).double(), non_blocking=True)
+            s64.copy_(slab.double(), non_blocking=True)
+            torch.cuda.synchronize()
+
+        e2e_step()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        dt = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda")
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": work / float(dt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(x64.numel() * 8 + b64.numel() * 8),
+               "d2h_bytes_per_step": int(p64.numel() * 8 + s64.numel() * 8),
+               "path": "per rank: pinned float64 -> device, DeviceScene P/BP on its view shard, "
+                       "NCCL reduce-scatter, its projections + z-slab back to pinned float64 "
+                       "(bytes per rank)",
+               "steps": e2e_steps}
 
     # ---- CGLS ms/iter (BASELINE metric, second half) ---------------------------
     cgls = None
