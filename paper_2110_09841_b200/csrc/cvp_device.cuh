@@ -62,7 +62,7 @@ struct CutRec {
     float A;       // cut area [mm^2]
     float g;       // b2 d0 / f: mm of z per detector row at the centroid depth
     float rho2;    // |centroid - source_xy|^2
-    float halfw;   // rectangle half-width (elevation correction)
+    float shw;     // (b2/f) |hw| halfw: elevation ramp half-width per row offset (0: none)
     float kc;      // chi2(zc) at this cut minus the column anchor, per mm of dz
     float tr_a;    // row half-range: h f/(b2 (d0 - dd)) ...
     float tr_b;    // ... + |dz| * f dd / (b2 d0 (d0 - dd))
@@ -241,7 +241,7 @@ __device__ int column_cuts(const ViewConst& vc, const Scene& sc, int i, int j, b
             r.A = A;
             r.g = b2f * d0;
             r.rho2 = rho2;
-            r.halfw = halfw;
+            r.shw = float(vc.b2_over_f) * fabsf(hw) * halfw;
             r.kc = fb2f * delta * fast_rcp(D0f * d0);
             const float dd = fabsf(hw) * halfw;
             const float dm = fast_rcp(d0 - dd);
@@ -279,27 +279,29 @@ __device__ __forceinline__ float clamp_mean_local(float alpha, float spread, flo
 }
 
 // Row walk of one voxel against one column cut (visit_rows, cvp.cpp:180-235)
-// in voxel-local float32: u = chi2(zc) - m_ref at the cut's centroid depth,
-// pm = pp2 - m_ref, dz = zc - s3, h = a3/2. emit(m, share * inv_r2) — the
+// in voxel-local float32: Mf = m_ref (integer row near chi2(zc), as float),
+// u = chi2(zc) - m_ref at the cut's centroid depth, pm = pp2 - m_ref,
+// dz = zc - s3, h = a3/2. emit(m, share * inv_r2) — the
 // caller multiplies by the cut area once per cut.
 template <bool CLAMP, class Emit>
-__device__ __forceinline__ void walk_rows(const CutRec& c, int m_ref, float u, float pm, float dz,
+__device__ __forceinline__ void walk_rows(const CutRec& c, float Mf, float u, float pm, float dz,
                                           float h, bool corrected, const bool per_row_r,
                                           float inv_r2_fixed, int rows, Emit&& emit) {
     // rows whose boundaries can intersect the (elevation-widened) voxel
     // (cvp.cpp:183-201): symmetric bound of the four corner chi2 values
     const float tr = c.tr_a + fabsf(dz) * c.tr_b + 1e-5f;
-    int m_first = m_ref + int(ceilf(u - tr - 0.5f));
-    int m_last = m_ref + int(floorf(u + tr + 0.5f));
+    // Mf: the anchor row m_ref as an exact integer-valued float
+    int m_first = int(ceilf(u - tr - 0.5f) + Mf);
+    int m_last = int(floorf(u + tr + 0.5f) + Mf);
     if (CLAMP) {
         m_first = max(m_first, 0);
         m_last = min(m_last, rows - 1);
     }
     if (m_first > m_last) return;
-    // spread of the elevation rectangle at boundary e: |beta(e)| * halfw with
-    // beta(e) = (b2/f) hw (pm - e) = (g / rho) (pm - e)
-    const float sh = corrected ? c.g * fast_rsqrt(c.rho2) * c.halfw : 0.f;
-    float e = float(m_first - m_ref) - 0.5f;  // chi2 boundary - m_ref
+    // spread of the elevation rectangle at boundary e: |beta(e)| halfw with
+    // beta(e) = (b2/f) hw (pm - e)  (cvp.cpp:205)
+    const float sh = corrected ? c.shw : 0.f;
+    float e = (float(m_first) - Mf) - 0.5f;  // chi2 boundary - m_ref
     float a_top = c.g * (u - e);
     float plain_top = clampf(a_top, -h, h);
     float t_top = clamp_mean_local(a_top, sh * fabsf(pm - e), h);
@@ -329,20 +331,67 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int m_ref, float u, f
 // float32 remainders u = chi2(zc) - m_ref, pm = pp2 - m_ref.
 template <bool EXACT>
 __device__ __forceinline__ void voxel_anchor(double pp2, double dz64, float dz, double Q0,
-                                             int& m_ref, float& u, float& pm) {
+                                             float& Mf, float& u, float& pm) {
     if (EXACT) {
         const double c = fma(-dz64, Q0, pp2);
         const double mr = rint(c);
-        m_ref = int(mr);
+        Mf = float(mr);
         u = float(c - mr);
         pm = float(pp2 - mr);
     } else {
         const float c = fmaf(-dz, float(Q0), float(pp2));
         const float mr = rintf(c);
-        m_ref = int(mr);
+        Mf = mr;
         u = c - mr;
         pm = float(pp2) - mr;
     }
+}
+
+// Column anchor for a whole brick column: chi2 of voxel k0 + kk at the
+// base-centre depth is c0 - kk * delta (delta = a3 f / (b2 D0)). Per column
+// (G-phase) c0 is split into an integer row M0 and a float32 remainder f0, and
+// delta into dh (18 significant bits, so kk * dh is exact for kk < 64) and
+// the float32 residual dl. Per voxel: P = kk dh (exact), I = rint(P),
+// F = P - I (exact), so chi2 - (M0 - I) = (f0 - F) - kk dl to ~1e-7 px with
+// no float64 arithmetic in the voxel loop.
+struct ColumnAnchor {
+    int M0;
+    float f0, dh, dl;
+};
+
+template <bool EXACT>
+__device__ __forceinline__ ColumnAnchor column_anchor(double pp2, double dz0, double Q0, double a3) {
+    ColumnAnchor a;
+    float delta_f;
+    double delta;
+    if (EXACT) {
+        const double c0 = fma(-dz0, Q0, pp2);
+        const double m0 = rint(c0);
+        a.M0 = int(m0);
+        a.f0 = float(c0 - m0);
+        delta = a3 * Q0;
+        delta_f = float(delta);
+    } else {
+        const float c0 = fmaf(-float(dz0), float(Q0), float(pp2));
+        const float m0 = rintf(c0);
+        a.M0 = int(m0);
+        a.f0 = c0 - m0;
+        delta_f = float(a3) * float(Q0);
+        delta = double(delta_f);
+    }
+    a.dh = __uint_as_float(__float_as_uint(delta_f) & 0xFFFFFFE0u);
+    a.dl = float(delta - double(a.dh));
+    return a;
+}
+
+__device__ __forceinline__ void anchor_at(const ColumnAnchor& a, float pp2f, float kk, float& Mf,
+                                          float& u, float& pm) {
+    const float P = kk * a.dh;  // exact
+    const float I = rintf(P);
+    const float F = P - I;      // exact
+    u = fmaf(-kk, a.dl, a.f0 - F);
+    Mf = float(a.M0) - I;
+    pm = pp2f - Mf;
 }
 
 }  // namespace cvpb

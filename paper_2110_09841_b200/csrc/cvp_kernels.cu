@@ -58,12 +58,11 @@ struct CvpParams {
 // Shared-memory layout (dynamic). Cut records are two float4 each so a warp
 // reads one record with two broadcast LDS.128.
 struct Smem {
-    float4 cutA[MAXC * NCOL];  // {A, g, rho2, halfw}
+    float4 cutA[MAXC * NCOL];  // {A, g, rho2, shw}
     float4 cutB[MAXC * NCOL];  // {kc, tr_a, tr_b, n (bits)}
-    double Q0[NCOL];
+    int4 anchor[NCOL];        // ColumnAnchor {M0, f0, dh, dl} of each column
     float rho2c[NCOL];
-    int count[NCOL];
-    int nz[NCOL];             // forward: column has a nonzero voxel in the brick
+    int count[NCOL];          // cuts per column (before the G-phase: nonzero flag)
     float vox[NCOL * MUS];    // forward: mu; backward: accumulators
     int tile_m0, tile_n0, tile_rows, tile_cols, tile_stride, tile_ok;
     float mu_abs_max;         // forward: max |mu| over the brick
@@ -106,7 +105,7 @@ __device__ __forceinline__ void red_s32(uint32_t a, int v) {
 }
 
 __device__ __forceinline__ void store_cut(Smem& s, int slot, const CutRec& r) {
-    s.cutA[slot] = make_float4(r.A, r.g, r.rho2, r.halfw);
+    s.cutA[slot] = make_float4(r.A, r.g, r.rho2, r.shw);
     s.cutB[slot] = make_float4(r.kc, r.tr_a, r.tr_b, __int_as_float(r.n));
 }
 
@@ -117,7 +116,7 @@ __device__ __forceinline__ CutRec load_cut(uint32_t sbase, int slot) {
     r.A = a.x;
     r.g = a.y;
     r.rho2 = a.z;
-    r.halfw = a.w;
+    r.shw = a.w;
     r.kc = b.x;
     r.tr_a = b.y;
     r.tr_b = b.z;
@@ -203,7 +202,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
 
     const size_t plane = size_t(sc.n1) * sc.n2;
     // Stage the brick's voxels: [column][k] with odd stride (bank-conflict free).
-    if (tid < NCOL) s.nz[tid] = 0;
+    if (tid < NCOL) s.count[tid] = 0;
     if (tid == 0) s.mu_abs_max = 0.f;
     __syncthreads();
     float abs_max = 0.f;
@@ -213,7 +212,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
         float val = 0.f;
         if (FWD && i < i1 && j < j1 && k < k1) {
             val = __ldg(p.vol_in + size_t(k) * plane + size_t(j) * sc.n1 + i);
-            if (val != 0.f) s.nz[c] = 1;
+            if (val != 0.f) s.count[c] = 1;
             abs_max = fmaxf(abs_max, fabsf(val));
         }
         s.vox[c * MUS + kk] = val;
@@ -240,7 +239,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
             const int c = tid;
             const int i = i0 + (c % BI), j = j0 + (c / BI);
             int cnt = 0;
-            if (i < i1 && j < j1 && (!FWD || s.nz[c])) {
+            if (i < i1 && j < j1 && (!FWD || s.count[c])) {
                 ColumnRec col;
                 cnt = column_cuts<EXACT>(vc, sc, i, j, true, corr, col, [&](const CutRec& r) {
                     if (cnt < MAXC) store_cut(s, cnt * NCOL + c, r);
@@ -250,7 +249,10 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                     atomicOr(p.err, kDevSourcePlane);
                     cnt = 0;
                 }
-                s.Q0[c] = col.Q0;
+                const ColumnAnchor an = column_anchor<EXACT>(
+                    vc.pp2, sc.minz + (k0 + 0.5) * sc.a3 - vc.s3, col.Q0, sc.a3);
+                s.anchor[c] = make_int4(an.M0, __float_as_int(an.f0), __float_as_int(an.dh),
+                                        __float_as_int(an.dl));
                 s.rho2c[c] = col.rho2c;
             }
             s.count[c] = cnt;
@@ -306,8 +308,9 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
             __syncthreads();
         }
         // ---- V-phase -----------------------------------------------------
-        const double pp2 = vc.pp2;
         const double dz64 = zc64 - vc.s3;
+        const float pp2f = float(vc.pp2);
+        const float kkf = float(lane);
         const float dz = EXACT ? float(dz64) : float(zc64) - float(vc.s3);
         const float dz2 = dz * dz;
         float* out_img = FWD ? p.proj_out + vloc * npx : nullptr;
@@ -323,22 +326,28 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                 if (!__any_sync(0xffffffffu, kvalid && mu != 0.f)) continue;
             }
             const bool active = kvalid && (!FWD || mu != 0.f);
-            int m_ref;
-            float u0, pm;
-            voxel_anchor<EXACT>(pp2, dz64, dz, lds_f64(sbase + uint32_t(offsetof(Smem, Q0)) + 8u * c),
-                                m_ref, u0, pm);
+            float Mf, u0, pm;
+            {
+                int4 a4;
+                asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(a4.x), "=r"(a4.y), "=r"(a4.z), "=r"(a4.w)
+                             : "r"(sbase + uint32_t(offsetof(Smem, anchor)) + 16u * c));
+                const ColumnAnchor an{a4.x, __int_as_float(a4.y), __int_as_float(a4.z),
+                                      __int_as_float(a4.w)};
+                anchor_at(an, pp2f, kkf, Mf, u0, pm);
+            }
             const float inv_r2_fixed =
                 per_row_r ? -1.f : fast_rcp(lds_f32(sbase + uint32_t(offsetof(Smem, rho2c)) + 4u * c) + dz2);
             float acc = 0.f;
             auto do_cut = [&](const CutRec& r) {
-                const bool corrected = corr && r.halfw > 0.f && dz2 > r.rho2 * 1e-28f;
+                const bool corrected = corr && r.shw > 0.f && dz2 > r.rho2 * 1e-28f;
                 const float u = fmaf(dz, r.kc, u0);
                 const int ccol = r.n - tn0;
                 const bool col_in = tile_ok && unsigned(ccol) < unsigned(tcols);
                 const uint32_t cbase = tbase + 4u * uint32_t(ccol * tstride - tm0);
                 const float wA = FWD ? mu * r.A * qs : r.A;
                 float cut_acc = 0.f;
-                walk_rows<true>(r, m_ref, u, pm, dz, h, corrected, per_row_r, inv_r2_fixed, rows,
+                walk_rows<true>(r, Mf, u, pm, dz, h, corrected, per_row_r, inv_r2_fixed, rows,
                                 [&](int m, float wr) {
                                     const bool in_tile =
                                         col_in && unsigned(m - tm0) < unsigned(trows);
@@ -480,12 +489,11 @@ __global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, i
         *n_out = 0;
         return;
     }
-    int m_ref;
-    float u0, pm;
-    voxel_anchor<EXACT>(vc.pp2, dz64, dz, col.Q0, m_ref, u0, pm);
+    float Mf, u0, pm;
+    voxel_anchor<EXACT>(vc.pp2, dz64, dz, col.Q0, Mf, u0, pm);
     const float inv_r2_fixed = per_row_r ? -1.f : fast_rcp(col.rho2c + dz * dz);
     column_cuts<EXACT>(vc, sc, i, j, clamp != 0, corr, col, [&](const CutRec& r) {
-        const bool corrected = corr && r.halfw > 0.f && dz * dz > r.rho2 * 1e-28f;
+        const bool corrected = corr && r.shw > 0.f && dz * dz > r.rho2 * 1e-28f;
         const float u = fmaf(dz, r.kc, u0);
         cur_n = r.n;
         cur_A = r.A;
@@ -505,13 +513,13 @@ __global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, i
             ++nrec2;
         };
         if (clamp) {
-            walk_rows<true>(r, m_ref, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
+            walk_rows<true>(r, Mf, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
                             sc.rows, take);
-            walk_rows<true>(r, m_ref, u, pm, dz, h, corrected, false, 1.f, sc.rows, take2);
+            walk_rows<true>(r, Mf, u, pm, dz, h, corrected, false, 1.f, sc.rows, take2);
         } else {
-            walk_rows<false>(r, m_ref, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
+            walk_rows<false>(r, Mf, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
                              sc.rows, take);
-            walk_rows<false>(r, m_ref, u, pm, dz, h, corrected, false, 1.f, sc.rows, take2);
+            walk_rows<false>(r, Mf, u, pm, dz, h, corrected, false, 1.f, sc.rows, take2);
         }
         for (int t = 0; t < nrec && t < 64; ++t) {
             if (count < cap) {
