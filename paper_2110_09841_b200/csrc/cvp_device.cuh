@@ -283,7 +283,10 @@ __device__ __forceinline__ float clamp_mean_local(float alpha, float spread, flo
 // u = chi2(zc) - m_ref at the cut's centroid depth, pm = pp2 - m_ref,
 // dz = zc - s3, h = a3/2. emit(m, share * inv_r2) — the
 // caller multiplies by the cut area once per cut.
-template <bool CLAMP, class Emit>
+// DENSE: emit every row of the range with max(share, 0) (branch-free; a zero
+// share contributes nothing) instead of only rows with share > 0 (the record
+// view of cvp.cpp:221).
+template <bool CLAMP, class Emit, bool DENSE = false>
 __device__ __forceinline__ void walk_rows(const CutRec& c, float Mf, float u, float pm, float dz,
                                           float h, bool corrected, const bool per_row_r,
                                           float inv_r2_fixed, int rows, Emit&& emit) {
@@ -314,13 +317,13 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, float Mf, float u, fl
         const float plain_bot = clampf(a_bot, -h, h);
         const float t_bot = clamp_mean_local(a_bot, sh * fabsf(pm - e), h);
         const float share = t_top - t_bot;
-        if (share > 0.f) {
+        if (DENSE || share > 0.f) {
             float inv_r2 = inv_r2_fixed;
             if (per_row_r) {
                 const float zr = fmaf(0.5f, plain_top + plain_bot, dz);
                 inv_r2 = fast_rcp(fmaf(zr, zr, c.rho2));
             }
-            emit(m, share * inv_r2);
+            emit(m, (DENSE ? fmaxf(share, 0.f) : share) * inv_r2);
         }
         t_top = t_bot;
         plain_top = plain_bot;

@@ -347,8 +347,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                 const uint32_t cbase = tbase + 4u * uint32_t(ccol * tstride - tm0);
                 const float wA = FWD ? mu * r.A * qs : r.A;
                 float cut_acc = 0.f;
-                walk_rows<true>(r, Mf, u, pm, dz, h, corrected, per_row_r, inv_r2_fixed, rows,
-                                [&](int m, float wr) {
+                auto emit = [&](int m, float wr) {
                                     const bool in_tile =
                                         col_in && unsigned(m - tm0) < unsigned(trows);
                                     if (FWD) {
@@ -368,7 +367,9 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                                                            wr, cut_acc);
                                         }
                                     }
-                                });
+                                };
+                walk_rows<true, decltype(emit)&, !FWD>(r, Mf, u, pm, dz, h, corrected, per_row_r,
+                                                       inv_r2_fixed, rows, emit);
                 if (!FWD) acc = fmaf(wA, cut_acc, acc);
             };
             if (active) {
