@@ -342,8 +342,16 @@ def main():
     views_here = v1 - v0
     alg_bytes = 4.0 * nvox * views_here  # 4 B per voxel-view
     achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    if os.path.exists(tp) and world == 1:
+        with open(tp) as f:
+            t = json.load(f).get(dom)
+        if t:
+            traffic = t["dram_read"] + t["dram_write"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None,
+                "frac": achieved / hbm, "traffic": traffic,
+                "traffic_source": "profiles/traffic_r01.json (ncu dram bytes, same launch)",
                 "kernel": dom, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "note": "4 B/voxel-view (SURVEY 8d); the kernel is issue-bound, see DESIGN.md"}
