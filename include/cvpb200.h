@@ -222,6 +222,15 @@ int cvpb_vec_xpby(cvpb_context* ctx, const float* s, double beta, float* p, size
 /* 1 if every element is finite (cgls check_finite, solver.cpp:60-65). */
 int cvpb_vec_all_finite(cvpb_context* ctx, const float* x, size_t n, int* out_host, void* stream);
 
+/* SART / OS-SART pieces (PAPER.md:443-445 uses OS-SART with these
+ * projectors): out = (b - ax) / rowsum where rowsum > eps,
+ * else 0; x += lambda * corr / colsum where colsum > eps, clamped at 0 when
+ * nonneg. */
+int cvpb_vec_sart_residual(cvpb_context* ctx, const float* b, const float* ax, const float* rowsum,
+                           float* out, size_t n, void* stream);
+int cvpb_vec_sart_update(cvpb_context* ctx, float* x, const float* corr, const float* colsum,
+                         double lambda, int nonneg, size_t n, void* stream);
+
 /* Device-resident CGLS (cgls, solver.cpp:55-106) over the context's scene.
  * projector: 0 = CVP (cvp_opts), 1 = Siddon-K (k_per_edge), 2 = TT.
  * d_b is the data (float32 stack, not modified), d_x receives the iterate;

@@ -16,8 +16,8 @@ from .operators import (CutVolumeRecord, CvpOptions, CvpPrecision, DeviceScene, 
                         backproject_cvp_into, backproject_siddon_k, backproject_siddon_k_into,
                         collect_cut_records, pixel_scale_cos, pixel_scale_exact, project_cvp,
                         project_cvp_into, project_siddon_k, project_siddon_k_into, scene_for)
-from .solver import (CglsResult, LinearOperatorPair, adjoint_test, cgls, cvp_pair,
-                     extinction_from_intensity, fill_uniform01, relative_projector_error,
+from .solver import (CglsResult, LinearOperatorPair, SartResult, adjoint_test, cgls, cvp_pair,
+                     extinction_from_intensity, fill_uniform01, os_sart, relative_projector_error,
                      siddon_pair, tt_pair)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -100,6 +100,8 @@ SIGNATURES = {
     "cvpb_vec_axpy": (C.c_int, [_vp, C.c_double, _vp, _vp, C.c_size_t, _vp]),
     "cvpb_vec_xpby": (C.c_int, [_vp, _vp, C.c_double, _vp, C.c_size_t, _vp]),
     "cvpb_vec_all_finite": (C.c_int, [_vp, _vp, C.c_size_t, _ip, _vp]),
+    "cvpb_vec_sart_residual": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_size_t, _vp]),
+    "cvpb_vec_sart_update": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, C.c_int, C.c_size_t, _vp]),
     "cvpb_cgls": (C.c_int, [_vp, C.c_int, _P(cvpb_cvp_options), C.c_int, _vp, _vp, C.c_int, _dp,
                             _vp]),
 }

@@ -1032,6 +1032,22 @@ int cvpb_vec_all_finite(cvpb_context* ctx, const float* x, size_t n, int* out_ho
     return CVPB_OK;
 }
 
+int cvpb_vec_sart_residual(cvpb_context* ctx, const float* b, const float* ax, const float* rowsum,
+                           float* out, size_t n, void* stream) {
+    CVPB_TRY(check_ctx(ctx, false));
+    CVPB_CUDA(cvpb::launch_sart_residual(b, ax, rowsum, out, n, 1e-30f,
+                                         static_cast<cudaStream_t>(stream)));
+    return CVPB_OK;
+}
+
+int cvpb_vec_sart_update(cvpb_context* ctx, float* x, const float* corr, const float* colsum,
+                         double lambda, int nonneg, size_t n, void* stream) {
+    CVPB_TRY(check_ctx(ctx, false));
+    CVPB_CUDA(cvpb::launch_sart_update(x, corr, colsum, float(lambda), nonneg, n, 1e-30f,
+                                       static_cast<cudaStream_t>(stream)));
+    return CVPB_OK;
+}
+
 // ---- device-resident CGLS (solver.cpp:55-106) ------------------------------------
 
 int cvpb_cgls(cvpb_context* ctx, int projector, const cvpb_cvp_options* cvp_opts, int k_per_edge,

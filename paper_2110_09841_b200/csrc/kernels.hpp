@@ -71,6 +71,10 @@ int dot_partials_count();
 cudaError_t launch_axpy(double alpha, const float* x, float* y, size_t n, cudaStream_t stream);
 cudaError_t launch_xpby(const float* s, double beta, float* p, size_t n, cudaStream_t stream);
 cudaError_t launch_all_finite(const float* x, size_t n, int* d_flag, cudaStream_t stream);
+cudaError_t launch_sart_residual(const float* b, const float* ax, const float* rowsum, float* out,
+                                 size_t n, float eps, cudaStream_t stream);
+cudaError_t launch_sart_update(float* x, const float* corr, const float* colsum, float lambda,
+                               int nonneg, size_t n, float eps, cudaStream_t stream);
 cudaError_t launch_f64_to_f32(const double* in, float* out, size_t n, cudaStream_t stream);
 cudaError_t launch_f32_to_f64(const float* in, double* out, size_t n, cudaStream_t stream);
 

@@ -89,6 +89,30 @@ __global__ void f32_to_f64_kernel(const float* __restrict__ in, double* __restri
         out[i] = double(in[i]);
 }
 
+// SART (Andersen & Kak) pieces: r = (b - Ax) / (A 1) where A 1 > eps, else 0;
+// x += lambda * (A^T r) / (A^T 1) where A^T 1 > eps, optionally clamped >= 0.
+__global__ void sart_residual_kernel(const float* __restrict__ b, const float* __restrict__ ax,
+                                     const float* __restrict__ rowsum, float* __restrict__ out,
+                                     size_t n, float eps) {
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+        const float w = rowsum[i];
+        out[i] = w > eps ? (b[i] - ax[i]) / w : 0.f;
+    }
+}
+
+__global__ void sart_update_kernel(float* __restrict__ x, const float* __restrict__ corr,
+                                   const float* __restrict__ colsum, float lambda, int nonneg,
+                                   size_t n, float eps) {
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+        const float w = colsum[i];
+        float v = x[i] + (w > eps ? lambda * corr[i] / w : 0.f);
+        if (nonneg) v = fmaxf(v, 0.f);
+        x[i] = v;
+    }
+}
+
 inline int grid_for(size_t n) {
     const size_t blocks = (n + kThreads - 1) / kThreads;
     return int(blocks < size_t(148 * 16) ? (blocks > 0 ? blocks : 1) : 148 * 16);
@@ -117,6 +141,18 @@ cudaError_t launch_xpby(const float* s, double beta, float* p, size_t n, cudaStr
 
 cudaError_t launch_all_finite(const float* x, size_t n, int* d_flag, cudaStream_t stream) {
     finite_kernel<<<grid_for(n), kThreads, 0, stream>>>(x, n, d_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sart_residual(const float* b, const float* ax, const float* rowsum, float* out,
+                                 size_t n, float eps, cudaStream_t stream) {
+    sart_residual_kernel<<<grid_for(n), kThreads, 0, stream>>>(b, ax, rowsum, out, n, eps);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sart_update(float* x, const float* corr, const float* colsum, float lambda,
+                               int nonneg, size_t n, float eps, cudaStream_t stream) {
+    sart_update_kernel<<<grid_for(n), kThreads, 0, stream>>>(x, corr, colsum, lambda, nonneg, n, eps);
     return cudaGetLastError();
 }
 

@@ -208,3 +208,85 @@ def cgls(pair: LinearOperatorPair, b: ProjectionStack, iterations: int, device: 
                 raise N.CvpbRuntimeError(f"CGLS diverged (non-finite iterate) at iteration {it}")
         res.append(math.sqrt(_dot(device, r.values, r.values)))
     return CglsResult(x, res)
+
+
+@dataclass
+class SartResult:
+    x: object
+    residual_norms: List[float] = field(default_factory=list)
+
+
+def os_sart(scene: DeviceScene, b, iterations: int, n_subsets: int = 1, lam: float = 1.0,
+            nonneg: bool = False, projector: str = "cvp", opts: CvpOptions = None,
+            k_per_edge: int = 1, track_residual: bool = True) -> SartResult:
+    """Ordered-subset SART (Andersen & Kak 1984; Kak & Slaney ch. 7) with the
+    device projector pair — the reconstruction loop the paper's KCT uses
+    (SURVEY §8 row f4).
+
+    Subsets interleave views (subset s = views s, s+S, s+2S, ...); internally
+    the views are reordered so each subset is a contiguous view range of one
+    resident scene. Per sub-iteration:
+        r = (b_S - A_S x) / (A_S 1),   x += lam * (A_S^T r) / (A_S^T 1)
+    with the two vector steps as fused device kernels (cvpb_vec_sart_*)."""
+    import torch
+    if iterations < 1:
+        raise InvalidArgument("sart needs at least one iteration")
+    V = scene.n_views
+    S = max(1, min(int(n_subsets), V))
+    order = [v for s in range(S) for v in range(s, V, S)]
+    bounds = []
+    pos = 0
+    for s in range(S):
+        cnt = len(range(s, V, S))
+        bounds.append((pos, cnt))
+        pos += cnt
+    sc = scene if order == list(range(V)) else DeviceScene(
+        scene.vol_geom, scene.det, [scene.views[i] for i in order], scene.device)
+    opts = opts or CvpOptions()
+    bt = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.asarray(b, dtype=np.float32))
+    bt = bt.reshape(V, scene.det.rows, scene.det.cols).to(sc._torch_device(), torch.float32)
+    bp = bt[torch.as_tensor(order, device=bt.device)].contiguous()
+
+    def P(x, out, vb, vc):
+        if projector == "cvp":
+            return sc.project_cvp(x, out, opts, view_begin=vb, view_count=vc)
+        if projector == "siddon":
+            return sc.project_siddon(x, k_per_edge, out, view_begin=vb, view_count=vc)
+        return sc.project_tt(x, out, view_begin=vb, view_count=vc)
+
+    def BP(p, out, vb, vc):
+        if projector == "cvp":
+            return sc.backproject_cvp(p, out, opts, view_begin=vb, view_count=vc)
+        if projector == "siddon":
+            return sc.backproject_siddon(p, k_per_edge, out, view_begin=vb, view_count=vc)
+        return sc.backproject_tt(p, out, view_begin=vb, view_count=vc)
+
+    ones_v = torch.ones(scene.vol_geom.shape(), device=bt.device)
+    rowsum = sc.new_stack()
+    colsum = []
+    for vb, vc in bounds:
+        P(ones_v, rowsum[vb:vb + vc], vb, vc)
+        cs = sc.new_volume()
+        BP(torch.ones_like(rowsum[vb:vb + vc]), cs, vb, vc)
+        colsum.append(cs)
+    x = sc.new_volume()
+    ax = sc.new_stack()
+    r = sc.new_stack()
+    corr = sc.new_volume()
+    L = N.lib()
+    st = _stream(None)
+    res = []
+    for _ in range(iterations):
+        for (vb, vc), cs in zip(bounds, colsum):
+            axs, rs, bs, ws = ax[vb:vb + vc], r[vb:vb + vc], bp[vb:vb + vc], rowsum[vb:vb + vc]
+            P(x, axs, vb, vc)
+            N.check(L.cvpb_vec_sart_residual(sc._h, _ptr(bs), _ptr(axs), _ptr(ws), _ptr(rs),
+                                             rs.numel(), st))
+            BP(rs, corr, vb, vc)
+            N.check(L.cvpb_vec_sart_update(sc._h, _ptr(x), _ptr(corr), _ptr(cs), float(lam),
+                                           int(bool(nonneg)), x.numel(), st))
+        if track_residual:
+            P(x, ax, 0, V)
+            r.copy_(bp).sub_(ax)
+            res.append(math.sqrt(sc.dot(r, r)))
+    return SartResult(x, res)
