@@ -308,10 +308,36 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, float Mf, float u, fl
     float a_top = c.g * (u - e);
     float plain_top = clampf(a_top, -h, h);
     float t_top = clamp_mean_local(a_top, sh * fabsf(pm - e), h);
+    int m = m_first;
+    if (DENSE) {
+        // Rows 1 and 2 in straight-line code (a voxel-cut spans 1-2 rows in
+        // the common case): no loop control, no divergence between 1- and
+        // 2-row lanes — a missing second row is emitted at m_first with
+        // weight 0.
+        auto row_inv = [&](float pt, float pb) {
+            if (!per_row_r) return inv_r2_fixed;
+            const float zr = fmaf(0.5f, pt + pb, dz);
+            return fast_rcp(fmaf(zr, zr, c.rho2));
+        };
+        const float e1 = e + 1.f, e2 = e + 2.f;
+        const float a1 = c.g * (u - e1), a2 = c.g * (u - e2);
+        const float p1 = clampf(a1, -h, h), p2 = clampf(a2, -h, h);
+        const float t1 = clamp_mean_local(a1, sh * fabsf(pm - e1), h);
+        const float t2 = clamp_mean_local(a2, sh * fabsf(pm - e2), h);
+        const bool two = m_last > m_first;
+        emit(m_first, fmaxf(t_top - t1, 0.f) * row_inv(plain_top, p1));
+        emit(two ? m_first + 1 : m_first,
+             two ? fmaxf(t1 - t2, 0.f) * row_inv(p1, p2) : 0.f);
+        if (m_last <= m_first + 1) return;
+        m = m_first + 2;
+        e = e2;
+        t_top = t2;
+        plain_top = p2;
+    }
     // not unrolled: rows per voxel-cut are 1-3 and differ across lanes; an
     // unrolled pair + remainder runs the remainder with ~2 active lanes
 #pragma unroll 1
-    for (int m = m_first; m <= m_last; ++m) {
+    for (; m <= m_last; ++m) {
         e += 1.f;
         const float a_bot = c.g * (u - e);
         const float plain_bot = clampf(a_bot, -h, h);
