@@ -352,7 +352,8 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                                         col_in && unsigned(m - tm0) < unsigned(trows);
                                     if (FWD) {
                                         if (in_tile) {
-                                            red_s32(cbase + 4u * m, __float2int_rn(wr * wA));
+                                            const int q = __float2int_rn(wr * wA);
+                                            if (q != 0) red_s32(cbase + 4u * m, q);
                                         } else {
                                             const size_t px = size_t(m) * cols + r.n;
                                             atomicAdd(out_img + px,
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                                         }
                                     }
                                 };
-                walk_rows<true, decltype(emit)&, !FWD>(r, Mf, u, pm, dz, h, corrected, per_row_r,
+                walk_rows<true, decltype(emit)&, true>(r, Mf, u, pm, dz, h, corrected, per_row_r,
                                                        inv_r2_fixed, rows, emit);
                 if (!FWD) acc = fmaf(wA, cut_acc, acc);
             };
