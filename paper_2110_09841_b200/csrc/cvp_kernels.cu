@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                                         } else {
                                             const size_t px = size_t(m) * cols + r.n;
                                             atomicAdd(out_img + px,
-                                                      mu * r.A * wr * __ldg(scale + px));
+                                                      mu * r.A * wr);
                                         }
                                     } else {
                                         if (in_tile) {
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                 const int q = itile[cc * tstride + r];
                 if (q != 0) {
                     const size_t px = size_t(tm0 + r) * cols + (tn0 + cc);
-                    atomicAdd(out_img + px, float(q) * inv_qs * __ldg(scale + px));
+                    atomicAdd(out_img + px, float(q) * inv_qs);
                 }
             }
         }
@@ -420,6 +420,19 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
             }
         }
     }
+}
+
+// Phase-2 scaling of the forward output (cvp.cpp:473-474), one streaming pass
+// after all bricks have merged: out[v][px] *= scale[slot(v)][px].
+__global__ void apply_scale_kernel(float* __restrict__ out, const float* __restrict__ scales,
+                                   const ViewConst* __restrict__ views, int view_begin,
+                                   size_t npx) {
+    const int v = blockIdx.y;
+    const float* sc = scales + size_t(views[view_begin + v].scale_slot) * npx;
+    float* o = out + size_t(v) * npx;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < npx;
+         i += size_t(gridDim.x) * blockDim.x)
+        o[i] *= __ldg(sc + i);
 }
 
 // Per-pixel phase-2 factors (ScaleCache, cvp.cpp:264-302) in float64, stored
@@ -642,8 +655,14 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
         e = cudaMemsetAsync(L.proj_out, 0, sizeof(float) * size_t(sc.rows) * sc.cols * L.view_count,
                             stream);
         if (e != cudaSuccess) return e;
-        return L.exact ? launch_opts<true, true>(p, grid, dyn, stream)
-                       : launch_opts<false, true>(p, grid, dyn, stream);
+        e = L.exact ? launch_opts<true, true>(p, grid, dyn, stream)
+                    : launch_opts<false, true>(p, grid, dyn, stream);
+        if (e != cudaSuccess) return e;
+        const size_t npx = size_t(sc.rows) * sc.cols;
+        const int bx = int(std::min<size_t>((npx + 255) / 256, 64));
+        apply_scale_kernel<<<dim3(bx, L.view_count), 256, 0, stream>>>(L.proj_out, L.scales, L.views,
+                                                                       L.view_begin, npx);
+        return cudaGetLastError();
     }
     return L.exact ? launch_opts<true, false>(p, grid, dyn, stream)
                    : launch_opts<false, false>(p, grid, dyn, stream);
