@@ -307,7 +307,13 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, float Mf, float u, fl
     float e = (float(m_first) - Mf) - 0.5f;  // chi2 boundary - m_ref
     float a_top = c.g * (u - e);
     float plain_top = clampf(a_top, -h, h);
-    float t_top = clamp_mean_local(a_top, sh * fabsf(pm - e), h);
+    // The top boundary of the row range lies above the voxel, its ramp
+    // included, in all but ~1e-4 of voxel-cuts (the range is built from the
+    // voxel's own corners): T = h exactly. The branch is warp-uniform in
+    // practice, so the clamp-mean runs only for the rare straddling lane.
+    const float s_top = sh * fabsf(pm - e);
+    float t_top = h;
+    if (a_top - s_top < h) t_top = clamp_mean_local(a_top, s_top, h);
     int m = m_first;
     if (DENSE) {
         // Rows 1 and 2 in straight-line code (a voxel-cut spans 1-2 rows in
