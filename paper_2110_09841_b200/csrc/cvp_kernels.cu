@@ -64,6 +64,7 @@ struct Smem {
     float rho2c[NCOL];
     int count[NCOL];          // cuts per column (before the G-phase: nonzero flag)
     float vox[NCOL * MUS];    // forward: mu; backward: accumulators
+    float* img;               // forward: this view's output image
     int tile_m0, tile_n0, tile_rows, tile_cols, tile_stride, tile_ok;
     float mu_abs_max;         // forward: max |mu| over the brick
     float qscale;             // forward: fixed-point scale of this (brick, view)
@@ -102,6 +103,19 @@ __device__ __forceinline__ void sts_f32(uint32_t a, float v) {
 }
 __device__ __forceinline__ void red_s32(uint32_t a, int v) {
     asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// red.shared.add only where pred != 0 and v != 0 (no branch around it)
+__device__ __forceinline__ void red_s32_if(uint32_t a, int v, int pred) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.s32 p, %2, 0;\n\t"
+        "setp.ne.and.s32 q, %1, 0, p;\n\t"
+        "@q red.shared.add.s32 [%0], %1;\n\t}" ::"r"(a), "r"(v), "r"(pred) : "memory");
+}
+__device__ __forceinline__ uint64_t lds_u64(uint32_t a) {
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
 }
 
 __device__ __forceinline__ void store_cut(Smem& s, int slot, const CutRec& r) {
@@ -285,6 +299,8 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
             s.tile_cols = tc;
             s.tile_stride = stride;
             s.tile_ok = (tr > 0 && tc > 0 && stride * tc <= p.tile_cap) ? 1 : 0;
+            const size_t vl = size_t(v - p.view_begin);
+            if (FWD) s.img = p.proj_out + vl * npx;
         }
         __syncthreads();
         const int tm0 = s.tile_m0, tn0 = s.tile_n0, trows = s.tile_rows, tcols = s.tile_cols;
@@ -313,8 +329,12 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
         const float kkf = float(lane);
         const float dz = EXACT ? float(dz64) : float(zc64) - float(vc.s3);
         const float dz2 = dz * dz;
-        float* out_img = FWD ? p.proj_out + vloc * npx : nullptr;
         const float qs = FWD ? s.qscale : 0.f;
+        // Forward: pixels outside the tile (tile overflow / detector edges) go
+        // straight to global memory; the view's image pointer is re-read from
+        // shared memory inside that rare branch so no 64-bit address stays
+        // live in the cut loop.
+        const uint32_t img_slot = sbase + uint32_t(offsetof(Smem, img));
         const float* in_img = FWD ? nullptr : p.proj_in + vloc * npx;
         for (int c = warp; c < NCOL; c += NWARP) {
             const int cnt = lds_s32(sbase + uint32_t(offsetof(Smem, count)) + 4u * c);
@@ -351,13 +371,11 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                                     const bool in_tile =
                                         col_in && unsigned(m - tm0) < unsigned(trows);
                                     if (FWD) {
-                                        if (in_tile) {
-                                            const int q = __float2int_rn(wr * wA);
-                                            if (q != 0) red_s32(cbase + 4u * m, q);
-                                        } else {
-                                            const size_t px = size_t(m) * cols + r.n;
-                                            atomicAdd(out_img + px,
-                                                      mu * r.A * wr);
+                                        red_s32_if(cbase + 4u * m, __float2int_rn(wr * wA),
+                                                   in_tile);
+                                        if (!in_tile) {
+                                            float* img = reinterpret_cast<float*>(lds_u64(img_slot));
+                                            atomicAdd(img + (size_t(m) * cols + r.n), mu * r.A * wr);
                                         }
                                     } else {
                                         if (in_tile) {
@@ -398,7 +416,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                 const int q = itile[cc * tstride + r];
                 if (q != 0) {
                     const size_t px = size_t(tm0 + r) * cols + (tn0 + cc);
-                    atomicAdd(out_img + px, float(q) * inv_qs);
+                    atomicAdd(s.img + px, float(q) * inv_qs);
                 }
             }
         }
