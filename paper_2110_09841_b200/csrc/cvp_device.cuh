@@ -287,24 +287,34 @@ __device__ __forceinline__ float clamp_mean_local(float alpha, float spread, flo
 // share contributes nothing) instead of only rows with share > 0 (the record
 // view of cvp.cpp:221).
 template <bool CLAMP, class Emit, bool DENSE = false>
-__device__ __forceinline__ void walk_rows(const CutRec& c, float Mf, float u, float pm, float dz,
-                                          float h, bool corrected, const bool per_row_r,
+__device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, float u, float pm,
+                                          float dz, float h, bool corrected, const bool per_row_r,
                                           float inv_r2_fixed, int rows, Emit&& emit) {
     // rows whose boundaries can intersect the (elevation-widened) voxel
     // (cvp.cpp:183-201): symmetric bound of the four corner chi2 values
     const float tr = c.tr_a + fabsf(dz) * c.tr_b + 1e-5f;
-    // Mf: the anchor row m_ref as an exact integer-valued float
-    int m_first = int(ceilf(u - tr - 0.5f) + Mf);
-    int m_last = int(floorf(u + tr + 0.5f) + Mf);
+    // Mi / Mf: the anchor row m_ref as int and as (exact) float. ceil/floor
+    // relative to it by the 1.5*2^23 rounding trick (directed-rounding FADD +
+    // integer subtract: no conversion-unit instructions). The offsets are
+    // clamped to +-2^21 rows; only a voxel touching the source plane spans
+    // more, and the detector clamp below then yields the same range.
+    constexpr float kMagic = 12582912.f;
+    constexpr int kMagicBits = 0x4B400000;
+    const float clo = __fadd_ru(fmaxf(u - tr - 0.5f, -2097152.f), kMagic);
+    const float chi = __fadd_rd(fminf(u + tr + 0.5f, 2097152.f), kMagic);
+    int m_first = Mi + (__float_as_int(clo) - kMagicBits);
+    int m_last = Mi + (__float_as_int(chi) - kMagicBits);
+    float e0 = clo - kMagic;  // m_first - m_ref, exact
     if (CLAMP) {
         m_first = max(m_first, 0);
         m_last = min(m_last, rows - 1);
+        e0 = fmaxf(e0, -Mf);
     }
     if (m_first > m_last) return;
     // spread of the elevation rectangle at boundary e: |beta(e)| halfw with
     // beta(e) = (b2/f) hw (pm - e)  (cvp.cpp:205)
     const float sh = corrected ? c.shw : 0.f;
-    float e = (float(m_first) - Mf) - 0.5f;  // chi2 boundary - m_ref
+    float e = e0 - 0.5f;  // chi2 boundary - m_ref
     float a_top = c.g * (u - e);
     float plain_top = clampf(a_top, -h, h);
     // The top boundary of the row range lies above the voxel, its ramp
@@ -366,16 +376,18 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, float Mf, float u, fl
 // float32 remainders u = chi2(zc) - m_ref, pm = pp2 - m_ref.
 template <bool EXACT>
 __device__ __forceinline__ void voxel_anchor(double pp2, double dz64, float dz, double Q0,
-                                             float& Mf, float& u, float& pm) {
+                                             int& Mi, float& Mf, float& u, float& pm) {
     if (EXACT) {
         const double c = fma(-dz64, Q0, pp2);
         const double mr = rint(c);
+        Mi = int(mr);
         Mf = float(mr);
         u = float(c - mr);
         pm = float(pp2 - mr);
     } else {
         const float c = fmaf(-dz, float(Q0), float(pp2));
         const float mr = rintf(c);
+        Mi = int(mr);
         Mf = mr;
         u = c - mr;
         pm = float(pp2) - mr;
@@ -419,12 +431,13 @@ __device__ __forceinline__ ColumnAnchor column_anchor(double pp2, double dz0, do
     return a;
 }
 
-__device__ __forceinline__ void anchor_at(const ColumnAnchor& a, float pp2f, float kk, float& Mf,
-                                          float& u, float& pm) {
+__device__ __forceinline__ void anchor_at(const ColumnAnchor& a, float pp2f, float kk, int& Mi,
+                                          float& Mf, float& u, float& pm) {
     const float P = kk * a.dh;  // exact
     const float I = rintf(P);
     const float F = P - I;      // exact
     u = fmaf(-kk, a.dl, a.f0 - F);
+    Mi = a.M0 - __float2int_rn(P);
     Mf = float(a.M0) - I;
     pm = pp2f - Mf;
 }

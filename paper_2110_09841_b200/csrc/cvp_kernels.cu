@@ -346,6 +346,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                 if (!__any_sync(0xffffffffu, kvalid && mu != 0.f)) continue;
             }
             const bool active = kvalid && (!FWD || mu != 0.f);
+            int Mi;
             float Mf, u0, pm;
             {
                 int4 a4;
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                              : "r"(sbase + uint32_t(offsetof(Smem, anchor)) + 16u * c));
                 const ColumnAnchor an{a4.x, __int_as_float(a4.y), __int_as_float(a4.z),
                                       __int_as_float(a4.w)};
-                anchor_at(an, pp2f, kkf, Mf, u0, pm);
+                anchor_at(an, pp2f, kkf, Mi, Mf, u0, pm);
             }
             const float inv_r2_fixed =
                 per_row_r ? -1.f : fast_rcp(lds_f32(sbase + uint32_t(offsetof(Smem, rho2c)) + 4u * c) + dz2);
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                                         }
                                     }
                                 };
-                walk_rows<true, decltype(emit)&, true>(r, Mf, u, pm, dz, h, corrected, per_row_r,
+                walk_rows<true, decltype(emit)&, true>(r, Mi, Mf, u, pm, dz, h, corrected, per_row_r,
                                                        inv_r2_fixed, rows, emit);
                 if (!FWD) acc = fmaf(wA, cut_acc, acc);
             };
@@ -522,8 +523,9 @@ __global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, i
         *n_out = 0;
         return;
     }
+    int Mi;
     float Mf, u0, pm;
-    voxel_anchor<EXACT>(vc.pp2, dz64, dz, col.Q0, Mf, u0, pm);
+    voxel_anchor<EXACT>(vc.pp2, dz64, dz, col.Q0, Mi, Mf, u0, pm);
     const float inv_r2_fixed = per_row_r ? -1.f : fast_rcp(col.rho2c + dz * dz);
     column_cuts<EXACT>(vc, sc, i, j, clamp != 0, corr, col, [&](const CutRec& r) {
         const bool corrected = corr && r.shw > 0.f && dz * dz > r.rho2 * 1e-28f;
@@ -546,13 +548,13 @@ __global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, i
             ++nrec2;
         };
         if (clamp) {
-            walk_rows<true>(r, Mf, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
+            walk_rows<true>(r, Mi, Mf, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
                             sc.rows, take);
-            walk_rows<true>(r, Mf, u, pm, dz, h, corrected, false, 1.f, sc.rows, take2);
+            walk_rows<true>(r, Mi, Mf, u, pm, dz, h, corrected, false, 1.f, sc.rows, take2);
         } else {
-            walk_rows<false>(r, Mf, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
+            walk_rows<false>(r, Mi, Mf, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
                              sc.rows, take);
-            walk_rows<false>(r, Mf, u, pm, dz, h, corrected, false, 1.f, sc.rows, take2);
+            walk_rows<false>(r, Mi, Mf, u, pm, dz, h, corrected, false, 1.f, sc.rows, take2);
         }
         for (int t = 0; t < nrec && t < 64; ++t) {
             if (count < cap) {
