@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstddef>
 #include <cstdio>
+#include <type_traits>
 
 #include "cvp_device.cuh"
 #include "kernels.hpp"
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
         __syncthreads();
         const int tm0 = s.tile_m0, tn0 = s.tile_n0, trows = s.tile_rows, tcols = s.tile_cols;
         const int tstride = s.tile_stride;
+        const int tm1 = tm0 + trows - 1;
         const bool tile_ok = s.tile_ok != 0;
         const float* scale = p.scales + size_t(vc.scale_slot) * npx;
         const size_t vloc = size_t(v - p.view_begin);
@@ -330,8 +332,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
         const float dz = EXACT ? float(dz64) : float(zc64) - float(vc.s3);
         const float dz2 = dz * dz;
         const float qs = FWD ? s.qscale : 0.f;
-        // Forward: pixels outside the tile (tile overflow / detector edges) go
-        // straight to global memory; the view's image pointer is re-read from
+        // Forward, off-tile cuts: the view's image pointer is re-read from
         // shared memory inside that rare branch so no 64-bit address stays
         // live in the cut loop.
         const uint32_t img_slot = sbase + uint32_t(offsetof(Smem, img));
@@ -360,41 +361,50 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
             const float inv_r2_fixed =
                 per_row_r ? -1.f : fast_rcp(lds_f32(sbase + uint32_t(offsetof(Smem, rho2c)) + 4u * c) + dz2);
             float acc = 0.f;
-            auto do_cut = [&](const CutRec& r) {
+            // One voxel-cut. TILE: the cut's column lies in the detector tile.
+            // Every row with a nonzero share then lies inside the tile (the
+            // footprint is conservative by >= 1 row, brick_footprint); rows
+            // the walk visits beyond it carry share 0 exactly (both boundary
+            // clamp-means saturate at +-h) and are clamped into the tile,
+            // so the emits need no bounds branch. Otherwise (tile overflow,
+            // column off the tile: warp-uniform, rare) emit to global memory.
+            auto do_cut = [&](const CutRec& r, auto tile_tag) {
+                constexpr bool TILE = decltype(tile_tag)::value;
                 const bool corrected = corr && r.shw > 0.f && dz2 > r.rho2 * 1e-28f;
                 const float u = fmaf(dz, r.kc, u0);
-                const int ccol = r.n - tn0;
-                const bool col_in = tile_ok && unsigned(ccol) < unsigned(tcols);
-                const uint32_t cbase = tbase + 4u * uint32_t(ccol * tstride - tm0);
+                const uint32_t cbase = tbase + 4u * uint32_t((r.n - tn0) * tstride - tm0);
                 const float wA = FWD ? mu * r.A * qs : r.A;
                 float cut_acc = 0.f;
                 auto emit = [&](int m, float wr) {
-                                    const bool in_tile =
-                                        col_in && unsigned(m - tm0) < unsigned(trows);
-                                    if (FWD) {
-                                        red_s32_if(cbase + 4u * m, __float2int_rn(wr * wA),
-                                                   in_tile);
-                                        if (!in_tile) {
-                                            float* img = reinterpret_cast<float*>(lds_u64(img_slot));
-                                            atomicAdd(img + (size_t(m) * cols + r.n), mu * r.A * wr);
-                                        }
-                                    } else {
-                                        if (in_tile) {
-                                            cut_acc = fmaf(lds_f32(cbase + 4u * m), wr, cut_acc);
-                                        } else {
-                                            const size_t px = size_t(m) * cols + r.n;
-                                            cut_acc = fmaf(__ldg(in_img + px) * __ldg(scale + px),
-                                                           wr, cut_acc);
-                                        }
-                                    }
-                                };
+                    if (TILE) {
+                        const uint32_t a = cbase + 4u * uint32_t(min(max(m, tm0), tm1));
+                        if (FWD)
+                            red_s32(a, __float2int_rn(wr * wA));
+                        else
+                            cut_acc = fmaf(lds_f32(a), wr, cut_acc);
+                    } else {
+                        const size_t px = size_t(m) * cols + r.n;
+                        if (FWD) {
+                            float* img = reinterpret_cast<float*>(lds_u64(img_slot));
+                            atomicAdd(img + px, mu * r.A * wr);
+                        } else {
+                            cut_acc = fmaf(__ldg(in_img + px) * __ldg(scale + px), wr, cut_acc);
+                        }
+                    }
+                };
                 walk_rows<true, decltype(emit)&, true>(r, Mi, Mf, u, pm, dz, h, corrected, per_row_r,
                                                        inv_r2_fixed, rows, emit);
                 if (!FWD) acc = fmaf(wA, cut_acc, acc);
             };
+            auto cut = [&](const CutRec& r) {
+                if (tile_ok && unsigned(r.n - tn0) < unsigned(tcols))
+                    do_cut(r, std::true_type{});
+                else
+                    do_cut(r, std::false_type{});
+            };
             if (active) {
                 const int ncached = min(cnt, MAXC);
-                for (int q = 0; q < ncached; ++q) do_cut(load_cut(sbase, q * NCOL + c));
+                for (int q = 0; q < ncached; ++q) cut(load_cut(sbase, q * NCOL + c));
             }
             if (cnt > MAXC) {
                 // rare overflow (pixels much smaller than voxels): recompute cuts >= MAXC
@@ -402,7 +412,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                 ColumnRec col;
                 int idx = 0;
                 column_cuts<EXACT>(vc, sc, i, j, true, corr, col, [&](const CutRec& r) {
-                    if (idx++ >= MAXC && active) do_cut(r);
+                    if (idx++ >= MAXC && active) cut(r);
                 });
             }
             if (!FWD && kvalid) sts_f32(vaddr, lds_f32(vaddr) + acc);
