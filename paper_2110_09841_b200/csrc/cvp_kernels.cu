@@ -65,7 +65,8 @@ struct Smem {
     float rho2c[NCOL];
     int count[NCOL];          // cuts per column (before the G-phase: nonzero flag)
     float vox[NCOL * MUS];    // forward: mu; backward: accumulators
-    float* img;               // forward: this view's output image
+    float* img;               // this view's image (forward: output, backward: input)
+    const float* scale;       // backward: this view's phase-2 factors
     int tile_m0, tile_n0, tile_rows, tile_cols, tile_stride, tile_ok;
     float mu_abs_max;         // forward: max |mu| over the brick
     float qscale;             // forward: fixed-point scale of this (brick, view)
@@ -301,7 +302,8 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
             s.tile_stride = stride;
             s.tile_ok = (tr > 0 && tc > 0 && stride * tc <= p.tile_cap) ? 1 : 0;
             const size_t vl = size_t(v - p.view_begin);
-            if (FWD) s.img = p.proj_out + vl * npx;
+            s.img = FWD ? p.proj_out + vl * npx : const_cast<float*>(p.proj_in) + vl * npx;
+            s.scale = p.scales + size_t(vc.scale_slot) * npx;
         }
         __syncthreads();
         const int tm0 = s.tile_m0, tn0 = s.tile_n0, trows = s.tile_rows, tcols = s.tile_cols;
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
         // shared memory inside that rare branch so no 64-bit address stays
         // live in the cut loop.
         const uint32_t img_slot = sbase + uint32_t(offsetof(Smem, img));
-        const float* in_img = FWD ? nullptr : p.proj_in + vloc * npx;
+        const uint32_t scale_slot = sbase + uint32_t(offsetof(Smem, scale));
         for (int c = warp; c < NCOL; c += NWARP) {
             const int cnt = lds_s32(sbase + uint32_t(offsetof(Smem, count)) + 4u * c);
             if (cnt == 0) continue;
@@ -388,7 +390,9 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                             float* img = reinterpret_cast<float*>(lds_u64(img_slot));
                             atomicAdd(img + px, mu * r.A * wr);
                         } else {
-                            cut_acc = fmaf(__ldg(in_img + px) * __ldg(scale + px), wr, cut_acc);
+                            const float* img = reinterpret_cast<const float*>(lds_u64(img_slot));
+                            const float* scl = reinterpret_cast<const float*>(lds_u64(scale_slot));
+                            cut_acc = fmaf(__ldg(img + px) * __ldg(scl + px), wr, cut_acc);
                         }
                     }
                 };
