@@ -245,7 +245,7 @@ __device__ int column_cuts(const ViewConst& vc, const Scene& sc, int i, int j, b
             r.kc = fb2f * delta * fast_rcp(D0f * d0);
             const float dd = fabsf(hw) * halfw;
             const float dm = fast_rcp(d0 - dd);
-            r.tr_a = h * fb2f * dm;
+            r.tr_a = fmaf(h * fb2f, dm, 1e-5f);
             r.tr_b = fb2f * dd * dm * fast_rcp(d0);
             on_cut(r);
             ++count;
@@ -279,49 +279,52 @@ __device__ __forceinline__ float clamp_mean_local(float alpha, float spread, flo
 }
 
 // Row walk of one voxel against one column cut (visit_rows, cvp.cpp:180-235)
-// in voxel-local float32: Mf = m_ref (integer row near chi2(zc), as float),
-// u = chi2(zc) - m_ref at the cut's centroid depth, pm = pp2 - m_ref,
-// dz = zc - s3, h = a3/2. emit(m, share * inv_r2) — the
-// caller multiplies by the cut area once per cut.
+// in voxel-local float32, with every chi2 quantity shifted by +1/2 so row
+// boundaries sit on integers: Mi / Mf = m_ref (integer row near chi2(zc), as
+// int and as exact float), uh = chi2(zc) - m_ref + 1/2 at the cut's centroid
+// depth, pmh = pp2 - m_ref + 1/2, dz = zc - s3, h = a3/2, sh = the cut's
+// elevation half-width factor when the elevation correction applies, else 0.
+// Row m spans the boundaries e' = m - m_ref and e' + 1 (chi2 = m -+ 1/2).
+// emit(m, share * inv_r2) — the caller multiplies by the cut area once per cut.
 // DENSE: emit every row of the range with max(share, 0) (branch-free; a zero
 // share contributes nothing) instead of only rows with share > 0 (the record
 // view of cvp.cpp:221).
 template <bool CLAMP, class Emit, bool DENSE = false>
-__device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, float u, float pm,
-                                          float dz, float h, bool corrected, const bool per_row_r,
+__device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, float uh, float pmh,
+                                          float dz, float h, float sh, const bool per_row_r,
                                           float inv_r2_fixed, int rows, Emit&& emit) {
     // rows whose boundaries can intersect the (elevation-widened) voxel
     // (cvp.cpp:183-201): symmetric bound of the four corner chi2 values
-    const float tr = c.tr_a + fabsf(dz) * c.tr_b + 1e-5f;
-    // Mi / Mf: the anchor row m_ref as int and as (exact) float. ceil/floor
-    // relative to it by the 1.5*2^23 rounding trick (directed-rounding FADD +
-    // integer subtract: no conversion-unit instructions). The offsets are
-    // clamped to +-2^21 rows; only a voxel touching the source plane spans
-    // more, and the detector clamp below then yields the same range.
+    // (tr_a carries the 1e-5 px slack)
+    const float tr = fmaf(fabsf(dz), c.tr_b, c.tr_a);
+    // m_first - m_ref = ceil(uh - tr) - 1, m_last - m_ref = floor(uh + tr) by
+    // the 1.5*2^23 rounding trick (directed-rounding FADD + integer subtract:
+    // no conversion-unit instructions). The offsets are clamped to +-2^21
+    // rows; only a voxel touching the source plane spans more, and the
+    // detector clamp below then yields the same range.
     constexpr float kMagic = 12582912.f;
     constexpr int kMagicBits = 0x4B400000;
-    const float clo = __fadd_ru(fmaxf(u - tr - 0.5f, -2097152.f), kMagic);
-    const float chi = __fadd_rd(fminf(u + tr + 0.5f, 2097152.f), kMagic);
+    const float clo = __fadd_ru(fmaxf(uh - tr, -2097152.f), kMagic - 1.f);
+    const float chi = __fadd_rd(fminf(uh + tr, 2097152.f), kMagic);
     int m_first = Mi + (__float_as_int(clo) - kMagicBits);
     int m_last = Mi + (__float_as_int(chi) - kMagicBits);
-    float e0 = clo - kMagic;  // m_first - m_ref, exact
+    float e = clo - kMagic;  // top boundary of row m_first, relative to m_ref (exact)
     if (CLAMP) {
         m_first = max(m_first, 0);
         m_last = min(m_last, rows - 1);
-        e0 = fmaxf(e0, -Mf);
+        e = fmaxf(e, -Mf);
     }
     if (m_first > m_last) return;
     // spread of the elevation rectangle at boundary e: |beta(e)| halfw with
     // beta(e) = (b2/f) hw (pm - e)  (cvp.cpp:205)
-    const float sh = corrected ? c.shw : 0.f;
-    float e = e0 - 0.5f;  // chi2 boundary - m_ref
-    float a_top = c.g * (u - e);
+    const float dtop = pmh - e;
+    float a_top = c.g * (uh - e);
     float plain_top = clampf(a_top, -h, h);
     // The top boundary of the row range lies above the voxel, its ramp
     // included, in all but ~1e-4 of voxel-cuts (the range is built from the
     // voxel's own corners): T = h exactly. The branch is warp-uniform in
     // practice, so the clamp-mean runs only for the rare straddling lane.
-    const float s_top = sh * fabsf(pm - e);
+    const float s_top = sh * fabsf(dtop);
     float t_top = h;
     if (a_top - s_top < h) t_top = clamp_mean_local(a_top, s_top, h);
     int m = m_first;
@@ -329,24 +332,23 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
         // Rows 1 and 2 in straight-line code (a voxel-cut spans 1-2 rows in
         // the common case): no loop control, no divergence between 1- and
         // 2-row lanes — a missing second row is emitted at m_first with
-        // weight 0.
+        // weight 0. Boundary k lies at e + k: alpha = a_top - k g.
         auto row_inv = [&](float pt, float pb) {
             if (!per_row_r) return inv_r2_fixed;
             const float zr = fmaf(0.5f, pt + pb, dz);
             return fast_rcp(fmaf(zr, zr, c.rho2));
         };
-        const float e1 = e + 1.f, e2 = e + 2.f;
-        const float a1 = c.g * (u - e1), a2 = c.g * (u - e2);
+        const float a1 = a_top - c.g, a2 = fmaf(-2.f, c.g, a_top);
         const float p1 = clampf(a1, -h, h), p2 = clampf(a2, -h, h);
-        const float t1 = clamp_mean_local(a1, sh * fabsf(pm - e1), h);
-        const float t2 = clamp_mean_local(a2, sh * fabsf(pm - e2), h);
+        const float t1 = clamp_mean_local(a1, sh * fabsf(dtop - 1.f), h);
+        const float t2 = clamp_mean_local(a2, sh * fabsf(dtop - 2.f), h);
         const bool two = m_last > m_first;
         emit(m_first, fmaxf(t_top - t1, 0.f) * row_inv(plain_top, p1));
         emit(two ? m_first + 1 : m_first,
              two ? fmaxf(t1 - t2, 0.f) * row_inv(p1, p2) : 0.f);
         if (m_last <= m_first + 1) return;
         m = m_first + 2;
-        e = e2;
+        e += 2.f;
         t_top = t2;
         plain_top = p2;
     }
@@ -355,9 +357,9 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
 #pragma unroll 1
     for (; m <= m_last; ++m) {
         e += 1.f;
-        const float a_bot = c.g * (u - e);
+        const float a_bot = c.g * (uh - e);
         const float plain_bot = clampf(a_bot, -h, h);
-        const float t_bot = clamp_mean_local(a_bot, sh * fabsf(pm - e), h);
+        const float t_bot = clamp_mean_local(a_bot, sh * fabsf(pmh - e), h);
         const float share = t_top - t_bot;
         if (DENSE || share > 0.f) {
             float inv_r2 = inv_r2_fixed;

@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
         const float kkf = float(lane);
         const float dz = EXACT ? float(dz64) : float(zc64) - float(vc.s3);
         const float dz2 = dz * dz;
+        const float dz2e28 = dz2 * 1e28f;  // rho2 < dz2e28  <=>  dz^2 > 1e-28 rho2
         const float qs = FWD ? s.qscale : 0.f;
         // Forward, off-tile cuts: the view's image pointer is re-read from
         // shared memory inside that rare branch so no 64-bit address stays
@@ -360,6 +361,8 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                                       __int_as_float(a4.w)};
                 anchor_at(an, pp2f, kkf, Mi, Mf, u0, pm);
             }
+            const float u0h = u0 + 0.5f, pmh = pm + 0.5f;
+            const float muq = mu * qs;  // forward: fixed-point scale folded into mu
             const float inv_r2_fixed =
                 per_row_r ? -1.f : fast_rcp(lds_f32(sbase + uint32_t(offsetof(Smem, rho2c)) + 4u * c) + dz2);
             float acc = 0.f;
@@ -372,10 +375,12 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
             // column off the tile: warp-uniform, rare) emit to global memory.
             auto do_cut = [&](const CutRec& r, auto tile_tag) {
                 constexpr bool TILE = decltype(tile_tag)::value;
-                const bool corrected = corr && r.shw > 0.f && dz2 > r.rho2 * 1e-28f;
-                const float u = fmaf(dz, r.kc, u0);
+                // elevation correction unless the voxel sits in the source
+                // plane (shw >= 0 always; shw = 0 makes it a no-op)
+                const float sh = (corr && r.rho2 < dz2e28) ? r.shw : 0.f;
+                const float uh = fmaf(dz, r.kc, u0h);
                 const uint32_t cbase = tbase + 4u * uint32_t((r.n - tn0) * tstride - tm0);
-                const float wA = FWD ? mu * r.A * qs : r.A;
+                const float wA = FWD ? muq * r.A : r.A;
                 float cut_acc = 0.f;
                 auto emit = [&](int m, float wr) {
                     if (TILE) {
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                         }
                     }
                 };
-                walk_rows<true, decltype(emit)&, true>(r, Mi, Mf, u, pm, dz, h, corrected, per_row_r,
+                walk_rows<true, decltype(emit)&, true>(r, Mi, Mf, uh, pmh, dz, h, sh, per_row_r,
                                                        inv_r2_fixed, rows, emit);
                 if (!FWD) acc = fmaf(wA, cut_acc, acc);
             };
@@ -542,8 +547,8 @@ __global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, i
     voxel_anchor<EXACT>(vc.pp2, dz64, dz, col.Q0, Mi, Mf, u0, pm);
     const float inv_r2_fixed = per_row_r ? -1.f : fast_rcp(col.rho2c + dz * dz);
     column_cuts<EXACT>(vc, sc, i, j, clamp != 0, corr, col, [&](const CutRec& r) {
-        const bool corrected = corr && r.shw > 0.f && dz * dz > r.rho2 * 1e-28f;
-        const float u = fmaf(dz, r.kc, u0);
+        const float shc = (corr && dz * dz > r.rho2 * 1e-28f) ? r.shw : 0.f;
+        const float uh = fmaf(dz, r.kc, u0 + 0.5f), pmh = pm + 0.5f;
         cur_n = r.n;
         cur_A = r.A;
         // pass 1: share * inv_r2; pass 2 (fixed inv_r2 = 1): share alone
@@ -562,13 +567,13 @@ __global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, i
             ++nrec2;
         };
         if (clamp) {
-            walk_rows<true>(r, Mi, Mf, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
+            walk_rows<true>(r, Mi, Mf, uh, pmh, dz, h, shc, per_row_r != 0, inv_r2_fixed,
                             sc.rows, take);
-            walk_rows<true>(r, Mi, Mf, u, pm, dz, h, corrected, false, 1.f, sc.rows, take2);
+            walk_rows<true>(r, Mi, Mf, uh, pmh, dz, h, shc, false, 1.f, sc.rows, take2);
         } else {
-            walk_rows<false>(r, Mi, Mf, u, pm, dz, h, corrected, per_row_r != 0, inv_r2_fixed,
+            walk_rows<false>(r, Mi, Mf, uh, pmh, dz, h, shc, per_row_r != 0, inv_r2_fixed,
                              sc.rows, take);
-            walk_rows<false>(r, Mi, Mf, u, pm, dz, h, corrected, false, 1.f, sc.rows, take2);
+            walk_rows<false>(r, Mi, Mf, uh, pmh, dz, h, shc, false, 1.f, sc.rows, take2);
         }
         for (int t = 0; t < nrec && t < 64; ++t) {
             if (count < cap) {
