@@ -262,6 +262,39 @@ __device__ int column_cuts(const ViewConst& vc, const Scene& sc, int i, int j, b
     return count;
 }
 
+// Packed fp32x2 arithmetic (FADD2 / FMUL2 / FFMA2 on sm_100): one issue slot
+// for two independent lanes of the row walk's boundary pairs.
+__device__ __forceinline__ uint64_t pk2(float2 v) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(uint64_t v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+    return upk2(d);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    uint64_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+    return upk2(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+    return upk2(d);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+    return upk2(d);
+}
+
 // Mean of clamp(alpha + beta*xi, -h, h) over xi in [-halfw, halfw]
 // (clamp_mean, cvp.cpp:161-175) in voxel-local coordinates, branch-free.
 // With spread s = |beta| halfw, mean over [alpha-s, alpha+s] of
@@ -333,19 +366,31 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
         // the common case): no loop control, no divergence between 1- and
         // 2-row lanes — a missing second row is emitted at m_first with
         // weight 0. Boundary k lies at e + k: alpha = a_top - k g.
-        auto row_inv = [&](float pt, float pb) {
-            if (!per_row_r) return inv_r2_fixed;
-            const float zr = fmaf(0.5f, pt + pb, dz);
-            return fast_rcp(fmaf(zr, zr, c.rho2));
-        };
-        const float a1 = a_top - c.g, a2 = fmaf(-2.f, c.g, a_top);
-        const float p1 = clampf(a1, -h, h), p2 = clampf(a2, -h, h);
-        const float t1 = clamp_mean_local(a1, sh * fabsf(dtop - 1.f), h);
-        const float t2 = clamp_mean_local(a2, sh * fabsf(dtop - 2.f), h);
+        // Both boundaries as fp32x2 pairs.
+        const float2 A = fma2(make_float2(-1.f, -2.f), make_float2(c.g, c.g),
+                              make_float2(a_top, a_top));  // alpha at e+1, e+2
+        const float p1 = clampf(A.x, -h, h), p2 = clampf(A.y, -h, h);
+        const float2 D = add2(make_float2(dtop, dtop), make_float2(-1.f, -2.f));
+        const float s1 = sh * fabsf(D.x), s2 = sh * fabsf(D.y);
+        const float2 AP = add2(A, make_float2(h, h)), AM = sub2(A, make_float2(h, h));
+        const float2 d1 = make_float2(fmaxf(s1 - fabsf(AP.x), 0.f), fmaxf(s2 - fabsf(AP.y), 0.f));
+        const float2 d2 = make_float2(fmaxf(s1 - fabsf(AM.x), 0.f), fmaxf(s2 - fabsf(AM.y), 0.f));
+        const float2 num = sub2(mul2(d1, d1), mul2(d2, d2));
+        const float2 rr = make_float2(fast_rcp(fmaxf(s1, 1e-30f)), fast_rcp(fmaxf(s2, 1e-30f)));
+        const float2 T = fma2(mul2(num, rr), make_float2(0.25f, 0.25f), make_float2(p1, p2));
+        const float t1 = T.x, t2 = T.y;
+        const float2 W = sub2(make_float2(t_top, t1), T);
+        float2 inv = make_float2(inv_r2_fixed, inv_r2_fixed);
+        if (per_row_r) {
+            const float2 Z = fma2(add2(make_float2(plain_top, p1), make_float2(p1, p2)),
+                                  make_float2(0.5f, 0.5f), make_float2(dz, dz));
+            const float2 Q = fma2(Z, Z, make_float2(c.rho2, c.rho2));
+            inv = make_float2(fast_rcp(Q.x), fast_rcp(Q.y));
+        }
+        const float2 WI = mul2(make_float2(fmaxf(W.x, 0.f), fmaxf(W.y, 0.f)), inv);
         const bool two = m_last > m_first;
-        emit(m_first, fmaxf(t_top - t1, 0.f) * row_inv(plain_top, p1));
-        emit(two ? m_first + 1 : m_first,
-             two ? fmaxf(t1 - t2, 0.f) * row_inv(p1, p2) : 0.f);
+        emit(m_first, WI.x);
+        emit(two ? m_first + 1 : m_first, two ? WI.y : 0.f);
         if (m_last <= m_first + 1) return;
         m = m_first + 2;
         e += 2.f;
