@@ -198,7 +198,10 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
     float* tile = reinterpret_cast<float*>(smem_raw + sizeof(Smem));
     int* itile = reinterpret_cast<int*>(tile);  // forward: fixed-point accumulators
-    const uint32_t sbase = saddr(smem_raw);
+    // opaque to the compiler, so it stays in a register instead of being
+    // re-derived from SR_CgaCtaId in every cut
+    uint32_t sbase;
+    asm volatile("mov.u32 %0, %1;" : "=r"(sbase) : "r"(saddr(smem_raw)));
     const uint32_t tbase = sbase + uint32_t(sizeof(Smem));  // detector tile
 
     const Scene& sc = p.sc;
