@@ -364,8 +364,8 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
     if (DENSE) {
         // Rows 1 and 2 in straight-line code (a voxel-cut spans 1-2 rows in
         // the common case): no loop control, no divergence between 1- and
-        // 2-row lanes — a missing second row is emitted at m_first with
-        // weight 0. Boundary k lies at e + k: alpha = a_top - k g.
+        // 2-row lanes — a missing second row is emitted at m_first + 1 with
+        // weight 0 (callers clamp its index). Boundary k lies at e + k: alpha = a_top - k g.
         // Both boundaries as fp32x2 pairs.
         const float2 A = fma2(make_float2(-1.f, -2.f), make_float2(c.g, c.g),
                               make_float2(a_top, a_top));  // alpha at e+1, e+2
@@ -390,7 +390,7 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
         const float2 WI = mul2(make_float2(fmaxf(W.x, 0.f), fmaxf(W.y, 0.f)), inv);
         const bool two = m_last > m_first;
         emit(m_first, WI.x);
-        emit(two ? m_first + 1 : m_first, two ? WI.y : 0.f);
+        emit(m_first + 1, two ? WI.y : 0.f);  // may lie past m_last (and the detector): weight 0
         if (m_last <= m_first + 1) return;
         m = m_first + 2;
         e += 2.f;

@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
         __syncthreads();
         const int tm0 = s.tile_m0, tn0 = s.tile_n0, trows = s.tile_rows, tcols = s.tile_cols;
         const int tstride = s.tile_stride;
-        const int tm1 = tm0 + trows - 1;
+        const uint32_t trm1 = uint32_t(trows - 1);
         const bool tile_ok = s.tile_ok != 0;
         const float* scale = p.scales + size_t(vc.scale_slot) * npx;
         const size_t vloc = size_t(v - p.view_begin);
@@ -382,18 +382,21 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                 // plane (shw >= 0 always; shw = 0 makes it a no-op)
                 const float sh = (corr && r.rho2 < dz2e28) ? r.shw : 0.f;
                 const float uh = fmaf(dz, r.kc, u0h);
-                const uint32_t cbase = tbase + 4u * uint32_t((r.n - tn0) * tstride - tm0);
+                const uint32_t cbase = tbase + 4u * uint32_t((r.n - tn0) * tstride);
                 const float wA = FWD ? muq * r.A : r.A;
                 float cut_acc = 0.f;
                 auto emit = [&](int m, float wr) {
                     if (TILE) {
-                        const uint32_t a = cbase + 4u * uint32_t(min(max(m, tm0), tm1));
+                        // rows off the tile (either side) carry share 0: any
+                        // in-tile slot will do, so one unsigned min clamps both
+                        const uint32_t a = cbase + 4u * min(uint32_t(m - tm0), trm1);
                         if (FWD)
                             red_s32(a, __float2int_rn(wr * wA));
                         else
                             cut_acc = fmaf(lds_f32(a), wr, cut_acc);
                     } else {
-                        const size_t px = size_t(m) * cols + r.n;
+                        // the walk's padding emit may sit one row past the detector
+                        const size_t px = size_t(min(m, rows - 1)) * cols + r.n;
                         if (FWD) {
                             float* img = reinterpret_cast<float*>(lds_u64(img_slot));
                             atomicAdd(img + px, mu * r.A * wr);
