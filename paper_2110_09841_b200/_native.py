@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcvpb200.so")
+# CVPB_LIB: developer override (kernel-variant experiments); defaults to the in-tree build
+LIB_PATH = os.environ.get("CVPB_LIB") or os.path.join(HERE, "libcvpb200.so")
 
 
 class cvpb_volume_geometry(C.Structure):

@@ -444,7 +444,7 @@ __device__ __forceinline__ void voxel_anchor(double pp2, double dz64, float dz, 
 // Column anchor for a whole brick column: chi2 of voxel k0 + kk at the
 // base-centre depth is c0 - kk * delta (delta = a3 f / (b2 D0)). Per column
 // (G-phase) c0 is split into an integer row M0 and a float32 remainder f0, and
-// delta into dh (18 significant bits, so kk * dh is exact for kk < 64) and
+// delta into dh (17 significant bits, so kk * dh is exact for kk < 128) and
 // the float32 residual dl. Per voxel: P = kk dh (exact), I = rint(P),
 // F = P - I (exact), so chi2 - (M0 - I) = (f0 - F) - kk dl to ~1e-7 px with
 // no float64 arithmetic in the voxel loop.
@@ -473,7 +473,7 @@ __device__ __forceinline__ ColumnAnchor column_anchor(double pp2, double dz0, do
         delta_f = float(a3) * float(Q0);
         delta = double(delta_f);
     }
-    a.dh = __uint_as_float(__float_as_uint(delta_f) & 0xFFFFFFE0u);
+    a.dh = __uint_as_float(__float_as_uint(delta_f) & 0xFFFFFFC0u);
     a.dl = float(delta - double(a.dh));
     return a;
 }

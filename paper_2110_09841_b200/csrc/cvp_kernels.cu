@@ -32,10 +32,38 @@ namespace cvpb {
 
 namespace {
 
-constexpr int BI = 16, BJ = 16, BK = 32;
-constexpr int NCOL = BI * BJ;           // 256 columns per brick
-constexpr int NT = 256;                 // threads per CTA
+#ifndef CVP_BJ
+#define CVP_BJ 8
+#endif
+#ifndef CVP_BK
+#define CVP_BK 64
+#endif
+constexpr int BI = 16, BJ = CVP_BJ, BK = CVP_BK;
+constexpr int NCOL = BI * BJ;           // voxel columns per brick
+#ifndef CVP_NT
+#define CVP_NT 256
+#endif
+constexpr int NT = CVP_NT;              // threads per CTA
 constexpr int NWARP = NT / 32;
+constexpr int NH = BK / 32;             // voxels per lane along x3 (lane, lane + 32, ...)
+static_assert(BK % 32 == 0 && BK <= 128, "anchor split is exact for kk < 128");
+static_assert(NCOL <= NT, "one G-phase thread per column");
+#ifndef CVP_MINB
+#define CVP_MINB 3                      // resident CTAs per SM (80 registers)
+#endif
+#ifndef CVP_NV
+#define CVP_NV 2
+#endif
+constexpr int NV = CVP_NV;              // voxels per lane per cut pass (kk = lane + 32 t)
+static_assert(NH % NV == 0, "whole voxel groups per column");
+
+// Per-lane state of one voxel in the V-phase.
+struct VoxState {
+    int Mi;
+    float Mf, u0h, pmh, dz, dz2e28, mu, muq, inv_r2_fixed, acc;
+    uint32_t vaddr;
+    bool kvalid, active;
+};
 constexpr int MAXC = 4;                 // cuts cached per column; more are recomputed
 constexpr int MUS = BK + 1;             // padded column stride of the voxel tile
 
@@ -193,7 +221,7 @@ __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene
 // CORR: elevation correction option; CCR: CutCentroid radius estimate
 // (cvp.hpp:17-22) — compile-time so the unused paths cost no registers.
 template <bool EXACT, bool FWD, bool CORR, bool CCR>
-__global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
+__global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
     float* tile = reinterpret_cast<float*>(smem_raw + sizeof(Smem));
@@ -246,15 +274,12 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
     const size_t npx = size_t(rows) * cols;
     const float h = p.h;
     constexpr bool corr = CORR, per_row_r = CCR;
-    const int k = k0 + lane;
-    const bool kvalid = k < k1;
-    const double zc64 = sc.minz + (k + 0.5) * sc.a3;
 
     for (int v = vg0; v < vg1; ++v) {
         const ViewConst& vc = p.views[v];
         __syncthreads();  // previous view's V-phase / flush is complete
         // ---- G-phase: column cuts --------------------------------------
-        {
+        if (tid < NCOL) {
             const int c = tid;
             const int i = i0 + (c % BI), j = j0 + (c / BI);
             int cnt = 0;
@@ -331,44 +356,54 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
             __syncthreads();
         }
         // ---- V-phase -----------------------------------------------------
-        const double dz64 = zc64 - vc.s3;
         const float pp2f = float(vc.pp2);
-        const float kkf = float(lane);
-        const float dz = EXACT ? float(dz64) : float(zc64) - float(vc.s3);
-        const float dz2 = dz * dz;
-        const float dz2e28 = dz2 * 1e28f;  // rho2 < dz2e28  <=>  dz^2 > 1e-28 rho2
         const float qs = FWD ? s.qscale : 0.f;
         // Forward, off-tile cuts: the view's image pointer is re-read from
         // shared memory inside that rare branch so no 64-bit address stays
         // live in the cut loop.
         const uint32_t img_slot = sbase + uint32_t(offsetof(Smem, img));
         const uint32_t scale_slot = sbase + uint32_t(offsetof(Smem, scale));
-        for (int c = warp; c < NCOL; c += NWARP) {
+        // Each lane carries NV voxels of one column through every cut (NV = NH
+        // with CVP_PAIR: the cut record, tile test and loop control are shared
+        // by the lane's voxels kk = lane and lane + 32).
+        for (int ch = warp; ch < NCOL * NH / NV; ch += NWARP) {
+            constexpr int NG = NH / NV;  // voxel groups per column
+            const int c = ch / NG;
+            const int hf0 = (ch % NG) * NV;
             const int cnt = lds_s32(sbase + uint32_t(offsetof(Smem, count)) + 4u * c);
             if (cnt == 0) continue;
-            const uint32_t vaddr = sbase + uint32_t(offsetof(Smem, vox)) + 4u * (c * MUS + lane);
-            float mu = 0.f;
-            if (FWD) {
-                mu = lds_f32(vaddr);
-                if (!__any_sync(0xffffffffu, kvalid && mu != 0.f)) continue;
+            int4 a4;
+            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(a4.x), "=r"(a4.y), "=r"(a4.z), "=r"(a4.w)
+                         : "r"(sbase + uint32_t(offsetof(Smem, anchor)) + 16u * c));
+            const ColumnAnchor an{a4.x, __int_as_float(a4.y), __int_as_float(a4.z),
+                                  __int_as_float(a4.w)};
+            VoxState vs[NV];
+            bool any_active = false;
+#pragma unroll
+            for (int t = 0; t < NV; ++t) {
+                VoxState& v = vs[t];
+                const int kk = lane + 32 * (hf0 + t);
+                const int k = k0 + kk;
+                v.kvalid = k < k1;
+                const double zc64 = sc.minz + (k + 0.5) * sc.a3;
+                v.dz = EXACT ? float(zc64 - vc.s3) : float(zc64) - float(vc.s3);
+                v.dz2e28 = v.dz * v.dz * 1e28f;  // rho2 < dz2e28  <=>  dz^2 > 1e-28 rho2
+                v.vaddr = sbase + uint32_t(offsetof(Smem, vox)) + 4u * (c * MUS + kk);
+                v.mu = FWD ? lds_f32(v.vaddr) : 0.f;
+                v.active = v.kvalid && (!FWD || v.mu != 0.f);
+                any_active |= v.active;
+                float u0, pm;
+                anchor_at(an, pp2f, float(kk), v.Mi, v.Mf, u0, pm);
+                v.u0h = u0 + 0.5f;
+                v.pmh = pm + 0.5f;
+                v.muq = v.mu * qs;  // forward: fixed-point scale folded into mu
+                v.inv_r2_fixed = per_row_r ? -1.f
+                                           : fast_rcp(lds_f32(sbase + uint32_t(offsetof(Smem, rho2c)) + 4u * c) +
+                                                      v.dz * v.dz);
+                v.acc = 0.f;
             }
-            const bool active = kvalid && (!FWD || mu != 0.f);
-            int Mi;
-            float Mf, u0, pm;
-            {
-                int4 a4;
-                asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(a4.x), "=r"(a4.y), "=r"(a4.z), "=r"(a4.w)
-                             : "r"(sbase + uint32_t(offsetof(Smem, anchor)) + 16u * c));
-                const ColumnAnchor an{a4.x, __int_as_float(a4.y), __int_as_float(a4.z),
-                                      __int_as_float(a4.w)};
-                anchor_at(an, pp2f, kkf, Mi, Mf, u0, pm);
-            }
-            const float u0h = u0 + 0.5f, pmh = pm + 0.5f;
-            const float muq = mu * qs;  // forward: fixed-point scale folded into mu
-            const float inv_r2_fixed =
-                per_row_r ? -1.f : fast_rcp(lds_f32(sbase + uint32_t(offsetof(Smem, rho2c)) + 4u * c) + dz2);
-            float acc = 0.f;
+            if (FWD && !__any_sync(0xffffffffu, any_active)) continue;
             // One voxel-cut. TILE: the cut's column lies in the detector tile.
             // Every row with a nonzero share then lies inside the tile (the
             // footprint is conservative by >= 1 row, brick_footprint); rows
@@ -376,14 +411,14 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
             // clamp-means saturate at +-h) and are clamped into the tile,
             // so the emits need no bounds branch. Otherwise (tile overflow,
             // column off the tile: warp-uniform, rare) emit to global memory.
-            auto do_cut = [&](const CutRec& r, auto tile_tag) {
+            auto do_cut = [&](const CutRec& r, VoxState& v, auto tile_tag) {
                 constexpr bool TILE = decltype(tile_tag)::value;
                 // elevation correction unless the voxel sits in the source
                 // plane (shw >= 0 always; shw = 0 makes it a no-op)
-                const float sh = (corr && r.rho2 < dz2e28) ? r.shw : 0.f;
-                const float uh = fmaf(dz, r.kc, u0h);
+                const float sh = (corr && r.rho2 < v.dz2e28) ? r.shw : 0.f;
+                const float uh = fmaf(v.dz, r.kc, v.u0h);
                 const uint32_t cbase = tbase + 4u * uint32_t((r.n - tn0) * tstride);
-                const float wA = FWD ? muq * r.A : r.A;
+                const float wA = FWD ? v.muq * r.A : r.A;
                 float cut_acc = 0.f;
                 auto emit = [&](int m, float wr) {
                     if (TILE) {
@@ -399,7 +434,7 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                         const size_t px = size_t(min(m, rows - 1)) * cols + r.n;
                         if (FWD) {
                             float* img = reinterpret_cast<float*>(lds_u64(img_slot));
-                            atomicAdd(img + px, mu * r.A * wr);
+                            atomicAdd(img + px, v.mu * r.A * wr);
                         } else {
                             const float* img = reinterpret_cast<const float*>(lds_u64(img_slot));
                             const float* scl = reinterpret_cast<const float*>(lds_u64(scale_slot));
@@ -407,17 +442,22 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                         }
                     }
                 };
-                walk_rows<true, decltype(emit)&, true>(r, Mi, Mf, uh, pmh, dz, h, sh, per_row_r,
-                                                       inv_r2_fixed, rows, emit);
-                if (!FWD) acc = fmaf(wA, cut_acc, acc);
+                walk_rows<true, decltype(emit)&, true>(r, v.Mi, v.Mf, uh, v.pmh, v.dz, h, sh, per_row_r,
+                                                       v.inv_r2_fixed, rows, emit);
+                if (!FWD) v.acc = fmaf(wA, cut_acc, v.acc);
             };
             auto cut = [&](const CutRec& r) {
-                if (tile_ok && unsigned(r.n - tn0) < unsigned(tcols))
-                    do_cut(r, std::true_type{});
-                else
-                    do_cut(r, std::false_type{});
+                if (tile_ok && unsigned(r.n - tn0) < unsigned(tcols)) {
+#pragma unroll
+                    for (int t = 0; t < NV; ++t)
+                        if (vs[t].active) do_cut(r, vs[t], std::true_type{});
+                } else {
+#pragma unroll
+                    for (int t = 0; t < NV; ++t)
+                        if (vs[t].active) do_cut(r, vs[t], std::false_type{});
+                }
             };
-            if (active) {
+            if (any_active) {
                 const int ncached = min(cnt, MAXC);
                 for (int q = 0; q < ncached; ++q) cut(load_cut(sbase, q * NCOL + c));
             }
@@ -427,10 +467,14 @@ __global__ void __launch_bounds__(NT, 3) cvp_brick_kernel(CvpParams p) {
                 ColumnRec col;
                 int idx = 0;
                 column_cuts<EXACT>(vc, sc, i, j, true, corr, col, [&](const CutRec& r) {
-                    if (idx++ >= MAXC && active) cut(r);
+                    if (idx++ >= MAXC) cut(r);
                 });
             }
-            if (!FWD && kvalid) sts_f32(vaddr, lds_f32(vaddr) + acc);
+            if (!FWD) {
+#pragma unroll
+                for (int t = 0; t < NV; ++t)
+                    if (vs[t].kvalid) sts_f32(vs[t].vaddr, lds_f32(vs[t].vaddr) + vs[t].acc);
+            }
         }
         // ---- flush (forward) ----------------------------------------------
         if (FWD && tile_ok) {
@@ -648,7 +692,7 @@ cudaError_t launch_cvp_tile_need(const Scene& sc, const ViewConst* views, int n_
 namespace {
 // Shared-memory budget per CTA for three resident CTAs per SM (228 KB SM
 // carve-out, 1 KB reserved per CTA) and the hard cap for the detector tile.
-constexpr int kSmemBudget3 = (228 * 1024) / 3 - 1024;
+constexpr int kSmemBudget3 = (228 * 1024) / CVP_MINB - 1024;
 constexpr int kTileCapMax = 16384;
 }  // namespace
 
