@@ -338,6 +338,9 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
         const int tstride = s.tile_stride;
         const uint32_t trm1 = uint32_t(trows - 1);
         const bool tile_ok = s.tile_ok != 0;
+        // the brick's footprint misses the detector in this view: every
+        // record would be clamped away (cvp.cpp:183-201), nothing to do
+        if (trows == 0 || tcols == 0) continue;
         const float* scale = p.scales + size_t(vc.scale_slot) * npx;
         const size_t vloc = size_t(v - p.view_begin);
         // ---- tile prologue ----------------------------------------------
@@ -433,8 +436,12 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                         // the walk's padding emit may sit one row past the detector
                         const size_t px = size_t(min(m, rows - 1)) * cols + r.n;
                         if (FWD) {
-                            float* img = reinterpret_cast<float*>(lds_u64(img_slot));
-                            atomicAdd(img + px, v.mu * r.A * wr);
+                            // zero records (padding row, empty range, mu = 0)
+                            // skip the global atomic
+                            if (wr != 0.f && v.mu != 0.f) {
+                                float* img = reinterpret_cast<float*>(lds_u64(img_slot));
+                                atomicAdd(img + px, v.mu * r.A * wr);
+                            }
                         } else {
                             const float* img = reinterpret_cast<const float*>(lds_u64(img_slot));
                             const float* scl = reinterpret_cast<const float*>(lds_u64(scale_slot));
@@ -448,9 +455,11 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             };
             auto cut = [&](const CutRec& r) {
                 if (tile_ok && unsigned(r.n - tn0) < unsigned(tcols)) {
+                    // tile path: inactive voxels run too, with zero weight
+                    // (forward: mu = 0) or a discarded accumulator (backward:
+                    // k past the volume), so there is no per-voxel branch
 #pragma unroll
-                    for (int t = 0; t < NV; ++t)
-                        if (vs[t].active) do_cut(r, vs[t], std::true_type{});
+                    for (int t = 0; t < NV; ++t) do_cut(r, vs[t], std::true_type{});
                 } else {
 #pragma unroll
                     for (int t = 0; t < NV; ++t)
