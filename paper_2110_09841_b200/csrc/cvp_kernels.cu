@@ -57,6 +57,11 @@ static_assert(NCOL <= NT, "one G-phase thread per column");
 constexpr int NV = CVP_NV;              // voxels per lane per cut pass (kk = lane + 32 t)
 static_assert(NH % NV == 0, "whole voxel groups per column");
 
+#ifndef CVP_SPLIT_FWD
+#define CVP_SPLIT_FWD 0
+#endif
+#define CVP_SPLIT_FWD_OK(fwd) (CVP_SPLIT_FWD || !(fwd))
+
 // Per-lane state of one voxel in the V-phase.
 struct VoxState {
     int Mi;
@@ -278,30 +283,29 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
     for (int v = vg0; v < vg1; ++v) {
         const ViewConst& vc = p.views[v];
         __syncthreads();  // previous view's V-phase / flush is complete
-        // ---- G-phase: column cuts --------------------------------------
-        if (tid < NCOL) {
-            const int c = tid;
-            const int i = i0 + (c % BI), j = j0 + (c / BI);
-            int cnt = 0;
-            if (i < i1 && j < j1 && (!FWD || s.count[c])) {
-                ColumnRec col;
-                cnt = column_cuts<EXACT>(vc, sc, i, j, true, corr, col, [&](const CutRec& r) {
-                    if (cnt < MAXC) store_cut(s, cnt * NCOL + c, r);
-                    ++cnt;
-                });
-                if (cnt < 0) {
-                    atomicOr(p.err, kDevSourcePlane);
-                    cnt = 0;
+        // ---- tile prologue: forward zeroes the fixed-point tile, backward
+        // stages the scaled image footprint (threads t0, t0 + step, ...) ----
+        auto tile_prologue = [&](int t0, int step) {
+            if (!s.tile_ok || s.tile_rows == 0 || s.tile_cols == 0) return;
+            const int tm0 = s.tile_m0, tn0 = s.tile_n0, trows = s.tile_rows, tcols = s.tile_cols;
+            const int tstride = s.tile_stride;
+            if (FWD) {
+                for (int idx = t0; idx < tstride * tcols; idx += step) itile[idx] = 0;
+            } else {
+                const float* img = s.img;
+                const float* scale = s.scale;
+                for (int idx = t0; idx < trows * tcols; idx += step) {
+                    const int r = idx / tcols, cc = idx % tcols;
+                    const size_t px = size_t(tm0 + r) * cols + (tn0 + cc);
+                    tile[cc * tstride + r] = __ldg(img + px) * __ldg(scale + px);
                 }
-                const ColumnAnchor an = column_anchor<EXACT>(
-                    vc.pp2, sc.minz + (k0 + 0.5) * sc.a3 - vc.s3, col.Q0, sc.a3);
-                s.anchor[c] = make_int4(an.M0, __float_as_int(an.f0), __float_as_int(an.dh),
-                                        __float_as_int(an.dl));
-                s.rho2c[c] = col.rho2c;
             }
-            s.count[c] = cnt;
-        }
-        if (tid == 0) {
+        };
+        // ---- G-phase: column cuts --------------------------------------
+        // Warps past the G-phase columns (NCOL < NT) compute the brick
+        // footprint and stage the detector tile meanwhile.
+        constexpr bool SPLIT = NCOL < NT && CVP_SPLIT_FWD_OK(FWD);
+        auto footprint = [&]() {
             int m0, m1, n0, n1;
             double dmin = 0.0, dmax = 0.0;
             brick_footprint(vc, sc, i0, i1, j0, j1, k0, k1, m0, m1, n0, n1, &dmin, &dmax);
@@ -332,7 +336,34 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             const size_t vl = size_t(v - p.view_begin);
             s.img = FWD ? p.proj_out + vl * npx : const_cast<float*>(p.proj_in) + vl * npx;
             s.scale = p.scales + size_t(vc.scale_slot) * npx;
+        };
+        if (tid < NCOL) {
+            const int c = tid;
+            const int i = i0 + (c % BI), j = j0 + (c / BI);
+            int cnt = 0;
+            if (i < i1 && j < j1 && (!FWD || s.count[c])) {
+                ColumnRec col;
+                cnt = column_cuts<EXACT>(vc, sc, i, j, true, corr, col, [&](const CutRec& r) {
+                    if (cnt < MAXC) store_cut(s, cnt * NCOL + c, r);
+                    ++cnt;
+                });
+                if (cnt < 0) {
+                    atomicOr(p.err, kDevSourcePlane);
+                    cnt = 0;
+                }
+                const ColumnAnchor an = column_anchor<EXACT>(
+                    vc.pp2, sc.minz + (k0 + 0.5) * sc.a3 - vc.s3, col.Q0, sc.a3);
+                s.anchor[c] = make_int4(an.M0, __float_as_int(an.f0), __float_as_int(an.dh),
+                                        __float_as_int(an.dl));
+                s.rho2c[c] = col.rho2c;
+            }
+            s.count[c] = cnt;
+        } else if (SPLIT) {
+            if (tid == NCOL) footprint();
+            asm volatile("bar.sync 1, %0;" ::"r"(NT - NCOL) : "memory");
+            tile_prologue(tid - NCOL, NT - NCOL);
         }
+        if (!SPLIT && tid == (NCOL < NT ? NCOL : 0)) footprint();
         __syncthreads();
         const int tm0 = s.tile_m0, tn0 = s.tile_n0, trows = s.tile_rows, tcols = s.tile_cols;
         const int tstride = s.tile_stride;
@@ -341,21 +372,8 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
         // the brick's footprint misses the detector in this view: every
         // record would be clamped away (cvp.cpp:183-201), nothing to do
         if (trows == 0 || tcols == 0) continue;
-        const float* scale = p.scales + size_t(vc.scale_slot) * npx;
-        const size_t vloc = size_t(v - p.view_begin);
-        // ---- tile prologue ----------------------------------------------
-        if (tile_ok) {
-            const int ntile = trows * tcols;
-            if (FWD) {
-                for (int idx = tid; idx < tstride * tcols; idx += NT) itile[idx] = 0;
-            } else {
-                const float* img = p.proj_in + vloc * npx;
-                for (int idx = tid; idx < ntile; idx += NT) {
-                    const int r = idx / tcols, cc = idx % tcols;
-                    const size_t px = size_t(tm0 + r) * cols + (tn0 + cc);
-                    tile[cc * tstride + r] = __ldg(img + px) * __ldg(scale + px);
-                }
-            }
+        if (!SPLIT && tile_ok) {
+            tile_prologue(tid, NT);
             __syncthreads();
         }
         // ---- V-phase -----------------------------------------------------

@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-ncu --set full --clock-control none --import-source on -k regex:cvp_brick -c 1 -o gpurun_out/prof_r01g_f python tools/prof_cvp.py --views 16 > gpurun_out/ncu_f.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:cvp_brick -s 1 -c 1 -o gpurun_out/prof_r01g_b python tools/prof_cvp.py --views 16 > gpurun_out/ncu_b.log 2>&1
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_r01g.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --cgls-iters 0 > gpurun_out/bench_ncu.log 2>&1
-ls -la gpurun_out
+ncu --set full --clock-control none --import-source on -k regex:cvp_brick -c 1 -o gpurun_out/prof_f python tools/prof_cvp.py --views 16 > gpurun_out/ncu_f.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:cvp_brick -s 1 -c 1 -o gpurun_out/prof_b python tools/prof_cvp.py --views 16 > gpurun_out/ncu_b.log 2>&1

@@ -6,10 +6,11 @@ set -e
 name=$1; shift
 cd "$(dirname "$0")/../paper_2110_09841_b200/csrc"
 B=../../build/csrc
-mkdir -p ../../build/variants
+O=../../build/variant_obj
+mkdir -p ../../build/variants $O
 /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC \
-  -I../../include -Xptxas -v --expt-relaxed-constexpr "$@" -c cvp_kernels.cu -o $B/cvp_kernels_$name.o 2> $B/cvp_kernels_$name.ptxas.txt \
-  || (cat $B/cvp_kernels_$name.ptxas.txt; false)
+  -I../../include -Xptxas -v --expt-relaxed-constexpr "$@" -c cvp_kernels.cu -o $O/cvp_kernels_$name.o 2> $O/cvp_kernels_$name.ptxas.txt \
+  || (cat $O/cvp_kernels_$name.ptxas.txt; false)
 /usr/local/cuda/bin/nvcc -shared -gencode arch=compute_100a,code=sm_100a -cudart static -o ../../build/variants/libcvpb200_$name.so \
-  $B/cvp_kernels_$name.o $B/siddon_kernels.o $B/tt_kernels.o $B/vecops.o $B/api.o
-grep -A2 "cvp_brick_kernelILb1ELb[01]ELb1ELb1E" $B/cvp_kernels_$name.ptxas.txt | grep -E "registers|spill"
+  $O/cvp_kernels_$name.o $B/siddon_kernels.o $B/tt_kernels.o $B/vecops.o $B/api.o
+grep -A2 "cvp_brick_kernelILb1ELb[01]ELb1ELb1E" $O/cvp_kernels_$name.ptxas.txt | grep -E "registers|spill"
