@@ -216,6 +216,12 @@ struct cvpb_context {
     DevBuf<int> d_rec_i;
     DevBuf<double> d_rec_d;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // host path: copy stream + per-chunk events (stack transfers overlap the
+    // projector launches of the neighbouring view chunks)
+    static constexpr int kChunks = 4;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_chunk[kChunks] = {};
+    cudaEvent_t ev_copy = nullptr;
     size_t nvox() const { return size_t(vol.counts[0]) * vol.counts[1] * vol.counts[2]; }
     size_t npx_view() const { return size_t(det.rows) * det.cols; }
 };
@@ -350,8 +356,17 @@ int ensure_host_buffers(cvpb_context* ctx) {
     CVPB_CUDA(ctx->h_vol.reserve(nv));
     CVPB_CUDA(ctx->h_proj.reserve(np));
     CVPB_CUDA(ctx->d_stage.reserve(std::max(nv, np)));
+    if (!ctx->copy_stream) {
+        CVPB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (cudaEvent_t& e : ctx->ev_chunk) CVPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CVPB_CUDA(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
+    }
     return CVPB_OK;
 }
+
+// View chunks of the host path: [begin, end) of chunk c out of n.
+int host_chunks(int nviews) { return nviews >= 32 ? cvpb_context::kChunks : 1; }
+int chunk_begin(int nviews, int n, int c) { return int((long long)nviews * c / n); }
 
 }  // namespace
 
@@ -432,6 +447,10 @@ void cvpb_context_destroy(cvpb_context* ctx) {
     ctx->d_rec_d.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    for (cudaEvent_t e : ctx->ev_chunk)
+        if (e) cudaEventDestroy(e);
+    if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -697,16 +716,28 @@ int cvpb_project_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
     CVPB_TRY(check_ctx(ctx));
     if (!volume || !proj) return fail(CVPB_INVALID_ARGUMENT, "null host buffer");
     CVPB_TRY(ensure_host_buffers(ctx));
-    cudaStream_t st = ctx->stream;
-    const size_t nv = ctx->nvox(), np = ctx->npx_view() * ctx->views.size();
+    cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
+    const size_t nv = ctx->nvox(), npx = ctx->npx_view();
     const int nviews = int(ctx->views.size());
     CVPB_CUDA(cudaEventRecord(ctx->ev0, st));
     CVPB_CUDA(cudaMemcpyAsync(ctx->d_stage.p, volume, sizeof(double) * nv, cudaMemcpyHostToDevice, st));
     CVPB_CUDA(cvpb::launch_f64_to_f32(ctx->d_stage.p, ctx->h_vol.p, nv, st));
-    CVPB_TRY(run_cvp(ctx, opts, exec, true, ctx->h_vol.p, nullptr, nullptr, ctx->h_proj.p, 0,
-                     nviews, 0, st));
-    CVPB_CUDA(cvpb::launch_f32_to_f64(ctx->h_proj.p, ctx->d_stage.p, np, st));
-    CVPB_CUDA(cudaMemcpyAsync(proj, ctx->d_stage.p, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+    // view chunks: chunk c's projections go back to the host (float64) on the
+    // copy stream while chunk c + 1 is projected
+    const int n = host_chunks(nviews);
+    for (int c = 0; c < n; ++c) {
+        const int v0 = chunk_begin(nviews, n, c), v1 = chunk_begin(nviews, n, c + 1);
+        const size_t off = npx * size_t(v0), cnt = npx * size_t(v1 - v0);
+        CVPB_TRY(run_cvp(ctx, opts, exec, true, ctx->h_vol.p, nullptr, nullptr, ctx->h_proj.p + off,
+                         v0, v1 - v0, 0, st));
+        CVPB_CUDA(cudaEventRecord(ctx->ev_chunk[c], st));
+        CVPB_CUDA(cudaStreamWaitEvent(cs, ctx->ev_chunk[c], 0));
+        CVPB_CUDA(cvpb::launch_f32_to_f64(ctx->h_proj.p + off, ctx->d_stage.p + off, cnt, cs));
+        CVPB_CUDA(cudaMemcpyAsync(proj + off, ctx->d_stage.p + off, sizeof(double) * cnt,
+                                  cudaMemcpyDeviceToHost, cs));
+    }
+    CVPB_CUDA(cudaEventRecord(ctx->ev_copy, cs));
+    CVPB_CUDA(cudaStreamWaitEvent(st, ctx->ev_copy, 0));
     CVPB_CUDA(cudaEventRecord(ctx->ev1, st));
     CVPB_TRY(device_error(ctx, st));
     if (view_seconds) {
@@ -723,14 +754,28 @@ int cvpb_backproject_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
     CVPB_TRY(check_ctx(ctx));
     if (!volume || !proj) return fail(CVPB_INVALID_ARGUMENT, "null host buffer");
     CVPB_TRY(ensure_host_buffers(ctx));
-    cudaStream_t st = ctx->stream;
-    const size_t nv = ctx->nvox(), np = ctx->npx_view() * ctx->views.size();
+    cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
+    const size_t nv = ctx->nvox(), npx = ctx->npx_view();
     const int nviews = int(ctx->views.size());
     CVPB_CUDA(cudaEventRecord(ctx->ev0, st));
-    CVPB_CUDA(cudaMemcpyAsync(ctx->d_stage.p, proj, sizeof(double) * np, cudaMemcpyHostToDevice, st));
-    CVPB_CUDA(cvpb::launch_f64_to_f32(ctx->d_stage.p, ctx->h_proj.p, np, st));
-    CVPB_TRY(run_cvp(ctx, opts, exec, false, nullptr, ctx->h_vol.p, ctx->h_proj.p, nullptr, 0,
-                     nviews, 0, st));
+    CVPB_CUDA(cudaStreamWaitEvent(cs, ctx->ev0, 0));
+    // view chunks: chunk c + 1 of the stack comes in (float64 -> float32) on
+    // the copy stream while chunk c is backprojected; chunks accumulate
+    const int n = host_chunks(nviews);
+    for (int c = 0; c < n; ++c) {
+        const int v0 = chunk_begin(nviews, n, c), v1 = chunk_begin(nviews, n, c + 1);
+        const size_t off = npx * size_t(v0), cnt = npx * size_t(v1 - v0);
+        CVPB_CUDA(cudaMemcpyAsync(ctx->d_stage.p + off, proj + off, sizeof(double) * cnt,
+                                  cudaMemcpyHostToDevice, cs));
+        CVPB_CUDA(cvpb::launch_f64_to_f32(ctx->d_stage.p + off, ctx->h_proj.p + off, cnt, cs));
+        CVPB_CUDA(cudaEventRecord(ctx->ev_chunk[c], cs));
+    }
+    for (int c = 0; c < n; ++c) {
+        const int v0 = chunk_begin(nviews, n, c), v1 = chunk_begin(nviews, n, c + 1);
+        CVPB_CUDA(cudaStreamWaitEvent(st, ctx->ev_chunk[c], 0));
+        CVPB_TRY(run_cvp(ctx, opts, exec, false, nullptr, ctx->h_vol.p,
+                         ctx->h_proj.p + npx * size_t(v0), nullptr, v0, v1 - v0, c > 0 ? 1 : 0, st));
+    }
     CVPB_CUDA(cvpb::launch_f32_to_f64(ctx->h_vol.p, ctx->d_stage.p, nv, st));
     CVPB_CUDA(cudaMemcpyAsync(volume, ctx->d_stage.p, sizeof(double) * nv, cudaMemcpyDeviceToHost, st));
     CVPB_CUDA(cudaEventRecord(ctx->ev1, st));

@@ -201,6 +201,22 @@ def test_host_path_matches_device_path():
     assert rel_l2(b_host.values, b_dev) < 1e-6
 
 
+def test_host_path_view_chunks_match_device_path():
+    # >= 32 views: the host path pipelines its stack transfers over view
+    # chunks (copy stream) and backprojects the chunks with accumulation
+    import paper_2110_09841_b200 as cb
+    geom, det, views, _ = make_case((24, 20, 28), (1.0, 1.0, 1.0), 40, 36, 1.0, 1.0, 60.0, 100.0, 37)
+    x64 = cb.fill_uniform01(geom.voxel_count(), 12)
+    vol = cb.AttenuationVolume(geom, x64)
+    p_host = cb.project_cvp(vol, views, det)
+    scene = cb.scene_for(geom, det, views)
+    p_dev = _np(scene.project_cvp(_torch_vol(x64, geom)))
+    assert rel_l2(p_host.values, p_dev) < 1e-6
+    b_host = cb.backproject_cvp(p_host, views, geom)
+    b_dev = _np(scene.backproject_cvp(scene.project_cvp(_torch_vol(x64, geom))))
+    assert rel_l2(b_host.values, b_dev) < 1e-6
+
+
 def test_scale_images_match_reference(reference):
     import paper_2110_09841_b200 as cb
     geom, det, views, sc = make_case((8, 8, 8), (1.0, 1.0, 1.0), 480, 616, 0.154, 0.154, 749.0,
