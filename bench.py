@@ -334,6 +334,33 @@ def main():
                 "how": "device-resident cvpb_cgls on the c3 scene (1 P + 1 BP + float64-accumulated "
                        "vector ops per iteration); ms/iter = (T(1+n) - T(1)) / n, wall clock "
                        "around synchronized calls"}
+    elif args.cgls_iters > 0:
+        # N > 1: view-sharded CGLS (parallel.distributed_cgls): x, s, p as
+        # z-slabs, r, q as view shards; all-gather of p before each P,
+        # reduce-scatter of the BP partials, all-reduced float64 scalars
+        from paper_2110_09841_b200 import parallel as par
+        op = par.scene_operator(scene, opts)
+        bt = op.project(x.reshape(-1))
+        vec = par.SceneVec(scene)
+
+        def run(n):
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            r = par.distributed_cgls(op, bt, n, vec)
+            torch.cuda.synchronize()
+            dist.barrier()
+            return time.perf_counter() - t0, r
+
+        ta, _ = run(1)
+        tb, r = run(1 + args.cgls_iters)
+        dt = torch.tensor([(tb - ta) / args.cgls_iters], device="cuda")
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        cgls = {"ms_per_iter": float(dt.item()) * 1e3, "iterations_timed": args.cgls_iters,
+                "residual_ratio": r.residual_norms[-1] / r.residual_norms[0],
+                "how": f"view-sharded CGLS over {world} ranks on the c3 scene (parallel."
+                       "distributed_cgls: slab-resident x/s/p, NCCL all-gather + reduce-scatter "
+                       "per iteration); ms/iter = (T(1+n) - T(1)) / n, max over ranks"}
 
     # ---- roofline of the dominant kernel -----------------------------------
     hbm, peak_src = _peaks()

@@ -115,3 +115,23 @@ def test_os_sart_reconstructs_the_blob():
     assert err6 < 0.2
     rn = cb.os_sart(scene, b, 2, n_subsets=4, nonneg=True)
     assert float(rn.x.min()) >= 0.0
+
+
+def test_scene_operator_distributed_cgls_single_rank_matches_device_cgls():
+    """parallel.scene_operator + distributed_cgls (the bench's N > 1 CGLS path)
+    on one rank, over the device scene and its vector kernels: same residual
+    history as the device-resident cvpb_cgls."""
+    import torch
+    import paper_2110_09841_b200 as cb
+    from paper_2110_09841_b200 import parallel as par
+    geom, det, views, _ = make_case((16, 12, 20), (1.0, 1.0, 1.0), 32, 28, 1.0, 1.0, 40.0, 70.0, 9)
+    scene = cb.DeviceScene(geom, det, views)
+    b = torch.from_numpy(cb.fill_uniform01(det.pixel_count() * 9, 5).astype(np.float32)).reshape(
+        9, 28, 32).cuda()
+    op = par.scene_operator(scene)
+    r = par.distributed_cgls(op, b, 5, par.SceneVec(scene))
+    x, res = scene.cgls(b, 5)
+    np.testing.assert_allclose(r.residual_norms, res, rtol=1e-5)
+    xs = r.x_slab[: geom.voxel_count()].double().cpu().numpy()
+    xd = x.double().cpu().numpy().ravel()
+    assert np.linalg.norm(xs - xd) <= 1e-4 * np.linalg.norm(xd)
