@@ -20,7 +20,7 @@
 //            stretched by the elevation of pixel row m seen at the voxel's
 //            projected column ("A1" uses the voxel-centre elevation instead).
 //
-// Execution mirrors the CVP bricks (cvp_kernels.cu): one CTA per 16x16x32
+// Execution mirrors the CVP bricks (cvp_kernels.cu): one CTA per 16x8x64
 // brick looping over views; per-column transaxial footprints computed once per
 // view (float64 anchors); per-voxel axial footprint in voxel-local float32;
 // forward accumulates into a shared detector tile, backward gathers from a
@@ -33,10 +33,12 @@ namespace cvpb {
 
 namespace {
 
-constexpr int BI = 16, BJ = 16, BK = 32;
+constexpr int BI = 16, BJ = 8, BK = 64;
 constexpr int NCOL = BI * BJ;
 constexpr int NT = 256;
 constexpr int NWARP = NT / 32;
+constexpr int NH = BK / 32;   // voxels per lane along x3
+static_assert(NCOL < NT, "warps past the columns stage the tile");
 constexpr int MAXN = 6;       // transaxial footprint width cached per column
 constexpr int MUS = BK + 1;
 
@@ -146,6 +148,45 @@ __device__ int column_footprint(const ViewConst& vc, const Scene& sc, int i, int
     return cnt;
 }
 
+// Transaxial footprint of a column too wide for the cache (cnt > MAXN): the
+// trapezoid in chi1 and the column range, re-derived per voxel.
+struct WideColumn {
+    float s0, s1, s2, s3;
+    int nr, nlo, nhi;
+};
+__device__ WideColumn wide_column(const ViewConst& vc, const Scene& sc, int i, int j) {
+    const double bcx = sc.minx + (i + 0.5) * sc.a1, bcy = sc.miny + (j + 0.5) * sc.a2;
+    const double Rx = bcx - vc.sx, Ry = bcy - vc.sy;
+    const double D0 = vc.w3x * Rx + vc.w3y * Ry;
+    const double X0 = (vc.w1x * Rx + vc.w1y * Ry) / D0;
+    WideColumn w;
+    w.nr = int(rint(X0));
+    const float x0 = float(X0 - w.nr), D0f = float(D0);
+    const float fu = float(vc.f / vc.b1);
+    const float ewx = float(vc.ew[0]), ewy = float(vc.ew[1]);
+    const float pp1r = float(vc.pp1 - w.nr);
+    const float Wx = fu * float(vc.eu[0]) + pp1r * ewx, Wy = fu * float(vc.eu[1]) + pp1r * ewy;
+    const float hx = float(0.5 * sc.a1), hy = float(0.5 * sc.a2);
+    float tau[4];
+    for (int q = 0; q < 4; ++q) {
+        const float px = (q == 1 || q == 2) ? hx : -hx, py = (q >= 2) ? hy : -hy;
+        tau[q] = (D0f * x0 + Wx * px + Wy * py) / (D0f + ewx * px + ewy * py);
+    }
+    w.s0 = tau[0];
+    w.s1 = tau[1];
+    w.s2 = tau[2];
+    w.s3 = tau[3];
+    sort4(w.s0, w.s1, w.s2, w.s3);
+    w.nlo = max(int(ceilf(w.s0 - 0.5f)), -w.nr);
+    w.nhi = min(int(floorf(w.s3 + 0.5f)), sc.cols - 1 - w.nr);
+    return w;
+}
+
+// One CTA per 16x8x64 brick looping over its views (the CVP brick layout,
+// cvp_kernels.cu): warps 0-3 compute the per-column transaxial footprints
+// while warps 4-7 bound the brick's detector footprint and stage the tile
+// (named barrier); each lane then carries the voxels kk = lane, lane + 32 of
+// a column through the axial walk.
 template <bool FWD>
 __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -174,13 +215,11 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
     }
     const int rows = sc.rows, cols = sc.cols;
     const size_t npx = size_t(rows) * cols;
-    const int k = k0 + lane;
-    const bool kvalid = k < k1;
-    const double zc64 = sc.minz + (k + 0.5) * sc.a3;
     for (int v = vg0; v < vg1; ++v) {
         const ViewConst& vc = p.views[v];
+        const size_t vloc = size_t(v - p.view_begin);
         __syncthreads();
-        {
+        if (tid < NCOL) {
             const int c = tid, i = i0 + (c % BI), j = j0 + (c / BI);
             int cnt = 0, nf = 0;
             if (i < i1 && j < j1) {
@@ -196,58 +235,65 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
             }
             s.n0[c] = nf;
             s.nn[c] = cnt;
-        }
-        if (tid == 0) {
-            // footprint rectangle of the brick (corner projections)
-            double cmin = INFINITY, cmax = -INFINITY, rmin = INFINITY, rmax = -INFINITY;
-            for (int q = 0; q < 8; ++q) {
-                const double x = sc.minx + ((q & 1) ? i1 : i0) * sc.a1 - vc.sx;
-                const double y = sc.miny + ((q & 2) ? j1 : j0) * sc.a2 - vc.sy;
-                const double z = sc.minz + ((q & 4) ? k1 : k0) * sc.a3 - vc.s3;
-                const double d = vc.w3x * x + vc.w3y * y;
-                const double c1 = (vc.w1x * x + vc.w1y * y) / d, c2 = vc.pp2 - z * vc.f_over_b2 / d;
-                cmin = fmin(cmin, c1);
-                cmax = fmax(cmax, c1);
-                rmin = fmin(rmin, c2);
-                rmax = fmax(rmax, c2);
+        } else {
+            if (tid == NCOL) {
+                // footprint rectangle of the brick (corner projections)
+                double cmin = INFINITY, cmax = -INFINITY, rmin = INFINITY, rmax = -INFINITY;
+                for (int q = 0; q < 8; ++q) {
+                    const double x = sc.minx + ((q & 1) ? i1 : i0) * sc.a1 - vc.sx;
+                    const double y = sc.miny + ((q & 2) ? j1 : j0) * sc.a2 - vc.sy;
+                    const double z = sc.minz + ((q & 4) ? k1 : k0) * sc.a3 - vc.s3;
+                    const double d = vc.w3x * x + vc.w3y * y;
+                    const double c1 = (vc.w1x * x + vc.w1y * y) / d, c2 = vc.pp2 - z * vc.f_over_b2 / d;
+                    cmin = fmin(cmin, c1);
+                    cmax = fmax(cmax, c1);
+                    rmin = fmin(rmin, c2);
+                    rmax = fmax(rmax, c2);
+                }
+                const int n0 = max(int(ceil(cmin - 0.5)) - 1, 0), n1 = min(int(floor(cmax + 0.5)) + 1, cols - 1);
+                const int m0 = max(int(ceil(rmin - 0.5)) - 1, 0), m1 = min(int(floor(rmax + 0.5)) + 1, rows - 1);
+                const int tr = max(m1 - m0 + 1, 0), tc = max(n1 - n0 + 1, 0);
+                s.tile_m0 = m0;
+                s.tile_n0 = n0;
+                s.tile_rows = tr;
+                s.tile_cols = tc;
+                s.tile_stride = tr | 1;
+                s.tile_ok = (tr > 0 && tc > 0 && (tr | 1) * tc <= p.tile_cap) ? 1 : 0;
             }
-            const int n0 = max(int(ceil(cmin - 0.5)) - 1, 0), n1 = min(int(floor(cmax + 0.5)) + 1, cols - 1);
-            const int m0 = max(int(ceil(rmin - 0.5)) - 1, 0), m1 = min(int(floor(rmax + 0.5)) + 1, rows - 1);
-            const int tr = max(m1 - m0 + 1, 0), tc = max(n1 - n0 + 1, 0);
-            s.tile_m0 = m0;
-            s.tile_n0 = n0;
-            s.tile_rows = tr;
-            s.tile_cols = tc;
-            s.tile_stride = tr | 1;
-            s.tile_ok = (tr > 0 && tc > 0 && (tr | 1) * tc <= p.tile_cap) ? 1 : 0;
+            asm volatile("bar.sync 1, %0;" ::"r"(NT - NCOL) : "memory");
+            if (s.tile_ok) {
+                const int tm0 = s.tile_m0, tn0 = s.tile_n0, trows = s.tile_rows, tcols = s.tile_cols;
+                const int tstride = s.tile_stride;
+                if (FWD) {
+                    for (int idx = tid - NCOL; idx < tstride * tcols; idx += NT - NCOL) tile[idx] = 0.f;
+                } else {
+                    const float* img = p.proj_in + vloc * npx;
+                    for (int idx = tid - NCOL; idx < trows * tcols; idx += NT - NCOL) {
+                        const int r = idx / tcols, cc = idx % tcols;
+                        tile[cc * tstride + r] = __ldg(img + size_t(tm0 + r) * cols + (tn0 + cc));
+                    }
+                }
+            }
         }
         __syncthreads();
         const int tm0 = s.tile_m0, tn0 = s.tile_n0, trows = s.tile_rows, tcols = s.tile_cols;
         const int tstride = s.tile_stride;
         const bool tile_ok = s.tile_ok != 0;
-        const size_t vloc = size_t(v - p.view_begin);
-        if (tile_ok) {
-            if (FWD) {
-                for (int idx = tid; idx < tstride * tcols; idx += NT) tile[idx] = 0.f;
-            } else {
-                const float* img = p.proj_in + vloc * npx;
-                for (int idx = tid; idx < trows * tcols; idx += NT) {
-                    const int r = idx / tcols, cc = idx % tcols;
-                    tile[cc * tstride + r] = __ldg(img + size_t(tm0 + r) * cols + (tn0 + cc));
-                }
-            }
-            __syncthreads();
-        }
-        const double dz64 = zc64 - vc.s3;
-        const float dz = float(dz64);
+        if (trows == 0 || tcols == 0) continue;  // the brick misses the detector in this view
         const float b2 = float(vc.b2);
         float* out_img = FWD ? p.proj_out + vloc * npx : nullptr;
         const float* in_img = FWD ? nullptr : p.proj_in + vloc * npx;
-        for (int c = warp; c < NCOL; c += NWARP) {
+        for (int cq = warp; cq < NCOL * NH; cq += NWARP) {
+            const int c = cq / NH, hf = cq % NH;
             const int cnt = s.nn[c];
             if (cnt == 0) continue;
-            const float mu = FWD ? s.vox[c * MUS + lane] : 0.f;
+            const int kk = lane + 32 * hf;
+            const int k = k0 + kk;
+            const bool kvalid = k < k1;
+            const float mu = FWD ? s.vox[c * MUS + kk] : 0.f;
             if (FWD && !__any_sync(0xffffffffu, kvalid && mu != 0.f)) continue;
+            const double dz64 = sc.minz + (k + 0.5) * sc.a3 - vc.s3;
+            const float dz = float(dz64);
             // anchor chi2(zc) at the base-centre depth (float64), split
             const double c0 = fma(-dz64, s.Q0[c], vc.pp2);
             const double mr = rint(c0);
@@ -263,12 +309,25 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
             const float2 amp = s.amp[c];
             const int nfirst = s.n0[c];
             const int ncache = min(cnt, MAXN);
+            // ramp reciprocals once per voxel (trap_cdf semantics: zero-width ramps)
+            const float w1 = t1 - t0, w3 = t3 - t2;
+            const float r1 = w1 > 0.f ? 0.5f * frcp(w1) : 0.f, r3 = w3 > 0.f ? 0.5f * frcp(w3) : 0.f;
+            auto cdf = [&](float x) {
+                const float c1 = fminf(fmaxf(x, t0), t1);
+                const float mid = fminf(fmaxf(x, t1), t2) - t1;
+                const float c3 = fminf(fmaxf(x, t2), t3);
+                return (c1 - t0) * (c1 - t0) * r1 + mid + (c3 - t2) * (w3 + t3 - c3) * r3;
+            };
+            const float ampA1 = amp.x * sqrtf(1.f + (u - pm) * (u - pm) * b2 * b2 * amp.y);
             float acc = 0.f;
-            if (kvalid && (!FWD || mu != 0.f) && cnt <= MAXN) {
-                float g_prev = trap_cdf(float(mf - m_ref) - 0.5f, t0, t1, t2, t3);
-                const float ampA1 = amp.x * sqrtf(1.f + (u - pm) * (u - pm) * b2 * b2 * amp.y);
+            const bool active = kvalid && (!FWD || mu != 0.f);
+            // the whole (rows x columns) footprint of this voxel inside the tile?
+            const bool inside = tile_ok && mf >= tm0 && ml < tm0 + trows && nfirst >= tn0 &&
+                                nfirst + ncache <= tn0 + tcols;
+            if (active && cnt <= MAXN) {
+                float g_prev = cdf(float(mf - m_ref) - 0.5f);
                 for (int m = mf; m <= ml; ++m) {
-                    const float g = trap_cdf(float(m - m_ref) + 0.5f, t0, t1, t2, t3);
+                    const float g = cdf(float(m - m_ref) + 0.5f);
                     const float f2 = g - g_prev;
                     g_prev = g;
                     if (!(f2 > 0.f)) continue;
@@ -280,68 +339,52 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
                         a = ampA1;
                     }
                     const float wrow = a * f2;
-                    for (int q = 0; q < ncache; ++q) {
-                        const int n = nfirst + q;
-                        const float w = wrow * s.f1[q * NCOL + c];
-                        const int r = m - tm0, cc = n - tn0;
-                        const bool in_tile = tile_ok && unsigned(r) < unsigned(trows) &&
-                                             unsigned(cc) < unsigned(tcols);
-                        if (FWD) {
-                            if (in_tile)
-                                atomicAdd(&tile[cc * tstride + r], mu * w);
+                    if (inside) {
+                        float* trow = tile + (nfirst - tn0) * tstride + (m - tm0);
+                        for (int q = 0; q < ncache; ++q) {
+                            const float w = wrow * s.f1[q * NCOL + c];
+                            if (FWD)
+                                atomicAdd(trow + q * tstride, mu * w);
                             else
-                                atomicAdd(out_img + size_t(m) * cols + n, mu * w);
-                        } else {
-                            acc += w * (in_tile ? tile[cc * tstride + r]
-                                                : __ldg(in_img + size_t(m) * cols + n));
+                                acc = fmaf(w, trow[q * tstride], acc);
+                        }
+                    } else {
+                        for (int q = 0; q < ncache; ++q) {
+                            const int n = nfirst + q;
+                            const float w = wrow * s.f1[q * NCOL + c];
+                            const int r = m - tm0, cc = n - tn0;
+                            const bool in_tile = tile_ok && unsigned(r) < unsigned(trows) &&
+                                                 unsigned(cc) < unsigned(tcols);
+                            if (FWD) {
+                                if (in_tile)
+                                    atomicAdd(&tile[cc * tstride + r], mu * w);
+                                else
+                                    atomicAdd(out_img + size_t(m) * cols + n, mu * w);
+                            } else {
+                                acc += w * (in_tile ? tile[cc * tstride + r]
+                                                    : __ldg(in_img + size_t(m) * cols + n));
+                            }
                         }
                     }
                 }
             }
-            if (cnt > MAXN && kvalid && (!FWD || mu != 0.f)) {
-                // very wide transaxial footprint: recompute the columns per voxel
-                const int i = i0 + (c % BI), j = j0 + (c / BI);
-                float f1[MAXN];
-                double Q0;
-                float4 axd;
-                float2 ampd;
-                int nf;
-                column_footprint(vc, sc, i, j, f1, nf, Q0, axd, ampd, p.amplitude);
-                // re-derive the trapezoid in t and walk every (n, m) pair directly
-                const double bcx = sc.minx + (i + 0.5) * sc.a1, bcy = sc.miny + (j + 0.5) * sc.a2;
-                const double Rx = bcx - vc.sx, Ry = bcy - vc.sy;
-                const double D0 = vc.w3x * Rx + vc.w3y * Ry;
-                const double X0 = (vc.w1x * Rx + vc.w1y * Ry) / D0;
-                const int nr = int(rint(X0));
-                const float x0 = float(X0 - nr), D0f = float(D0);
-                const float fu = float(vc.f / vc.b1);
-                const float ewx = float(vc.ew[0]), ewy = float(vc.ew[1]);
-                const float pp1r = float(vc.pp1 - nr);
-                const float Wx = fu * float(vc.eu[0]) + pp1r * ewx, Wy = fu * float(vc.eu[1]) + pp1r * ewy;
-                const float hx = float(0.5 * sc.a1), hy = float(0.5 * sc.a2);
-                float tau[4];
-                for (int q = 0; q < 4; ++q) {
-                    const float px = (q == 1 || q == 2) ? hx : -hx, py = (q >= 2) ? hy : -hy;
-                    tau[q] = (D0f * x0 + Wx * px + Wy * py) / (D0f + ewx * px + ewy * py);
-                }
-                float s0 = tau[0], s1 = tau[1], s2 = tau[2], s3 = tau[3];
-                sort4(s0, s1, s2, s3);
-                const int nlo = max(int(ceilf(s0 - 0.5f)), -nr), nhi = min(int(floorf(s3 + 0.5f)), cols - 1 - nr);
-                float g_prev = trap_cdf(float(mf - m_ref) - 0.5f, t0, t1, t2, t3);
+            if (cnt > MAXN && active) {
+                // very wide transaxial footprint: walk every (n, m) pair directly
+                const WideColumn wc = wide_column(vc, sc, i0 + (c % BI), j0 + (c / BI));
+                float g_prev = cdf(float(mf - m_ref) - 0.5f);
                 for (int m = mf; m <= ml; ++m) {
-                    const float g = trap_cdf(float(m - m_ref) + 0.5f, t0, t1, t2, t3);
+                    const float g = cdf(float(m - m_ref) + 0.5f);
                     const float f2 = g - g_prev;
                     g_prev = g;
                     if (!(f2 > 0.f)) continue;
                     const float vm = float(m - m_ref) - pm;
-                    const float a = p.amplitude ? amp.x * sqrtf(1.f + vm * vm * b2 * b2 * amp.y)
-                                                : amp.x * sqrtf(1.f + (u - pm) * (u - pm) * b2 * b2 * amp.y);
-                    float h_prev = trap_cdf(float(nlo) - 0.5f, s0, s1, s2, s3);
-                    for (int nn = nlo; nn <= nhi; ++nn) {
-                        const float hh = trap_cdf(float(nn) + 0.5f, s0, s1, s2, s3);
+                    const float a = p.amplitude ? amp.x * sqrtf(1.f + vm * vm * b2 * b2 * amp.y) : ampA1;
+                    float h_prev = trap_cdf(float(wc.nlo) - 0.5f, wc.s0, wc.s1, wc.s2, wc.s3);
+                    for (int nn = wc.nlo; nn <= wc.nhi; ++nn) {
+                        const float hh = trap_cdf(float(nn) + 0.5f, wc.s0, wc.s1, wc.s2, wc.s3);
                         const float w = a * f2 * (hh - h_prev);
                         h_prev = hh;
-                        const int n = nr + nn;
+                        const int n = wc.nr + nn;
                         if (FWD)
                             atomicAdd(out_img + size_t(m) * cols + n, mu * w);
                         else
@@ -349,7 +392,7 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
                     }
                 }
             }
-            if (!FWD && kvalid) s.vox[c * MUS + lane] += acc;
+            if (!FWD && kvalid) s.vox[c * MUS + kk] += acc;
         }
         if (FWD && tile_ok) {
             __syncthreads();
