@@ -33,12 +33,15 @@ namespace cvpb {
 namespace {
 
 #ifndef CVP_BJ
-#define CVP_BJ 8
+#define CVP_BJ 16
 #endif
 #ifndef CVP_BK
 #define CVP_BK 64
 #endif
-constexpr int BI = 16, BJ = CVP_BJ, BK = CVP_BK;
+#ifndef CVP_BI
+#define CVP_BI 8
+#endif
+constexpr int BI = CVP_BI, BJ = CVP_BJ, BK = CVP_BK;
 constexpr int NCOL = BI * BJ;           // voxel columns per brick
 #ifndef CVP_NT
 #define CVP_NT 256
