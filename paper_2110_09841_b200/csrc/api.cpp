@@ -207,6 +207,7 @@ struct cvpb_context {
     int n_slots = 0;
     int cvp_tile_need = 0;    // floats, largest brick footprint over the scene
     double r_min = 0.0;       // smallest source-to-volume-box distance over the views
+    double voxel_rows = 0.0;  // mean voxel height in detector rows at the volume centre
     DevBuf<ViewConst> d_views;
     DevBuf<float> d_scale_cos, d_scale_exact;
     DevBuf<int> d_err, d_box, d_flag;
@@ -309,6 +310,7 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     L.accumulate = accumulate;
     L.deterministic = exec ? exec->deterministic : 0;
     L.tile_need = ctx->cvp_tile_need;
+    L.tall_voxels = ctx->voxel_rows > 1.4 ? 1 : 0;
     L.err = ctx->d_err.p;
     if (!forward && view_count == 0 && !accumulate) {
         CVPB_CUDA(cudaMemsetAsync(vol_out, 0, sizeof(float) * ctx->nvox(), st));
@@ -522,6 +524,12 @@ int cvpb_set_geometry(cvpb_context* ctx, const cvpb_volume_geometry* vol,
         // corners and depth is affine, so checking the 4 box corners decides
         // the reference's per-voxel depth test (cvp.cpp:82-84) for all voxels
         const ViewConst& c = ctx->vconst[v];
+        {
+            // voxel height in detector rows at the depth of the volume centre
+            const double dc = c.w3x * (0.5 * (lo[0] + hi[0]) - c.sx) + c.w3y * (0.5 * (lo[1] + hi[1]) - c.sy);
+            const double rows_v = dc > 0.0 ? sc.a3 * c.f_over_b2 / dc : 0.0;
+            ctx->voxel_rows = v == 0 ? rows_v / n_views : ctx->voxel_rows + rows_v / n_views;
+        }
         for (int a = 0; a < 2; ++a)
             for (int b = 0; b < 2; ++b) {
                 const double px = (a ? hi[0] : lo[0]) - c.sx, py = (b ? hi[1] : lo[1]) - c.sy;

@@ -322,7 +322,10 @@ __device__ __forceinline__ float clamp_mean_local(float alpha, float spread, flo
 // DENSE: emit every row of the range with max(share, 0) (branch-free; a zero
 // share contributes nothing) instead of only rows with share > 0 (the record
 // view of cvp.cpp:221).
-template <bool CLAMP, class Emit, bool DENSE = false>
+// NR (DENSE only): rows walked in straight-line code before the loop — 2 for
+// voxels up to ~1 detector row tall, 3 for taller ones (the launch picks it
+// from the scene's largest voxel height in rows).
+template <bool CLAMP, class Emit, bool DENSE = false, int NR = 2>
 __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, float uh, float pmh,
                                           float dz, float h, float sh, const bool per_row_r,
                                           float inv_r2_fixed, int rows, Emit&& emit) {
@@ -403,11 +406,29 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
         const bool two = m_last > m_first;
         emit(m_first, CVP_DENSE_NORET && !nonempty ? 0.f : WI.x);
         emit(m_first + 1, two ? WI.y : 0.f);  // may lie past m_last (and the detector): weight 0
-        if (m_last <= m_first + 1) return;
-        m = m_first + 2;
-        e += 2.f;
-        t_top = t2;
-        plain_top = p2;
+        if constexpr (NR >= 3) {
+            // third row (boundary e + 3) in straight-line code as well
+            const float a3 = fmaf(-3.f, c.g, a_top);
+            const float p3 = clampf(a3, -h, h);
+            const float t3 = clamp_mean_local(a3, sh * fabsf(dtop - 3.f), h);
+            float inv3 = inv_r2_fixed;
+            if (per_row_r) {
+                const float z3 = fmaf(0.5f, p2 + p3, dz);
+                inv3 = fast_rcp(fmaf(z3, z3, c.rho2));
+            }
+            emit(m_first + 2, m_last > m_first + 1 ? fmaxf(t2 - t3, 0.f) * inv3 : 0.f);
+            if (m_last <= m_first + 2) return;
+            m = m_first + 3;
+            e += 3.f;
+            t_top = t3;
+            plain_top = p3;
+        } else {
+            if (m_last <= m_first + 1) return;
+            m = m_first + 2;
+            e += 2.f;
+            t_top = t2;
+            plain_top = p2;
+        }
     }
     // not unrolled: rows per voxel-cut are 1-3 and differ across lanes; an
     // unrolled pair + remainder runs the remainder with ~2 active lanes

@@ -228,7 +228,7 @@ __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene
 
 // CORR: elevation correction option; CCR: CutCentroid radius estimate
 // (cvp.hpp:17-22) — compile-time so the unused paths cost no registers.
-template <bool EXACT, bool FWD, bool CORR, bool CCR>
+template <bool EXACT, bool FWD, bool CORR, bool CCR, int NR>
 __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
@@ -470,8 +470,8 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                         }
                     }
                 };
-                walk_rows<true, decltype(emit)&, true>(r, v.Mi, v.Mf, uh, v.pmh, v.dz, h, sh, per_row_r,
-                                                       v.inv_r2_fixed, rows, emit);
+                walk_rows<true, decltype(emit)&, true, NR>(r, v.Mi, v.Mf, uh, v.pmh, v.dz, h, sh,
+                                                           per_row_r, v.inv_r2_fixed, rows, emit);
                 if (!FWD) v.acc = fmaf(wA, cut_acc, v.acc);
             };
             auto cut = [&](const CutRec& r) {
@@ -668,22 +668,25 @@ __global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, i
     *n_out = count;
 }
 
-template <bool EXACT, bool FWD, bool CORR, bool CCR>
+template <bool EXACT, bool FWD, bool CORR, bool CCR, int NR>
 cudaError_t launch_variant(const CvpParams& p, dim3 grid, int dyn, cudaStream_t stream) {
-    cudaError_t e = cudaFuncSetAttribute(cvp_brick_kernel<EXACT, FWD, CORR, CCR>,
+    cudaError_t e = cudaFuncSetAttribute(cvp_brick_kernel<EXACT, FWD, CORR, CCR, NR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
     if (e != cudaSuccess) return e;
-    cvp_brick_kernel<EXACT, FWD, CORR, CCR><<<grid, NT, dyn, stream>>>(p);
+    cvp_brick_kernel<EXACT, FWD, CORR, CCR, NR><<<grid, NT, dyn, stream>>>(p);
     return cudaGetLastError();
 }
 
+// Three straight-line rows only for the reference-default options (elevation
+// correction, CutCentroid radius); other option sets walk two.
 template <bool EXACT, bool FWD>
-cudaError_t launch_opts(const CvpParams& p, dim3 grid, int dyn, cudaStream_t stream) {
+cudaError_t launch_opts(const CvpParams& p, dim3 grid, int dyn, bool tall, cudaStream_t stream) {
     if (p.corr)
-        return p.per_row_r ? launch_variant<EXACT, FWD, true, true>(p, grid, dyn, stream)
-                           : launch_variant<EXACT, FWD, true, false>(p, grid, dyn, stream);
-    return p.per_row_r ? launch_variant<EXACT, FWD, false, true>(p, grid, dyn, stream)
-                       : launch_variant<EXACT, FWD, false, false>(p, grid, dyn, stream);
+        return p.per_row_r ? (tall ? launch_variant<EXACT, FWD, true, true, 3>(p, grid, dyn, stream)
+                                   : launch_variant<EXACT, FWD, true, true, 2>(p, grid, dyn, stream))
+                           : launch_variant<EXACT, FWD, true, false, 2>(p, grid, dyn, stream);
+    return p.per_row_r ? launch_variant<EXACT, FWD, false, true, 2>(p, grid, dyn, stream)
+                       : launch_variant<EXACT, FWD, false, false, 2>(p, grid, dyn, stream);
 }
 
 // Largest tile (odd row stride x columns) any brick needs under any view.
@@ -774,8 +777,8 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
         e = cudaMemsetAsync(L.proj_out, 0, sizeof(float) * size_t(sc.rows) * sc.cols * L.view_count,
                             stream);
         if (e != cudaSuccess) return e;
-        e = L.exact ? launch_opts<true, true>(p, grid, dyn, stream)
-                    : launch_opts<false, true>(p, grid, dyn, stream);
+        e = L.exact ? launch_opts<true, true>(p, grid, dyn, L.tall_voxels, stream)
+                    : launch_opts<false, true>(p, grid, dyn, L.tall_voxels, stream);
         if (e != cudaSuccess) return e;
         const size_t npx = size_t(sc.rows) * sc.cols;
         const int bx = int(std::min<size_t>((npx + 255) / 256, 64));
@@ -783,8 +786,8 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
                                                                        L.view_begin, npx);
         return cudaGetLastError();
     }
-    return L.exact ? launch_opts<true, false>(p, grid, dyn, stream)
-                   : launch_opts<false, false>(p, grid, dyn, stream);
+    return L.exact ? launch_opts<true, false>(p, grid, dyn, L.tall_voxels, stream)
+                   : launch_opts<false, false>(p, grid, dyn, L.tall_voxels, stream);
 }
 
 cudaError_t launch_scale_image(double f, double pp1, double pp2, double b1, double b2, int rows,

@@ -20,6 +20,7 @@ struct CvpLaunch {
     int forward, exact, elevation_correction, cut_centroid;
     int accumulate, deterministic;
     int tile_need;            // largest brick footprint (floats), see launch_cvp_tile_need
+    int tall_voxels;          // voxels ~2 detector rows tall: three straight-line rows
     int* err;                 // device error flag
 };
 
