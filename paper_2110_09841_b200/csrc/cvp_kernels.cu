@@ -51,6 +51,7 @@ constexpr int NWARP = NT / 32;
 constexpr int NH = BK / 32;             // voxels per lane along x3 (lane, lane + 32, ...)
 static_assert(BK % 32 == 0 && BK <= 128, "anchor split is exact for kk < 128");
 static_assert(NCOL <= NT, "one G-phase thread per column");
+static_assert(NT - BK >= NCOL, "per-layer dz threads lie outside the G-phase");
 #ifndef CVP_MINB
 #define CVP_MINB 3                      // resident CTAs per SM (80 registers)
 #endif
@@ -99,6 +100,7 @@ struct Smem {
     float4 cutB[MAXC * NCOL];  // {kc, tr_a, tr_b, n (bits)}
     int4 anchor[NCOL];        // ColumnAnchor {M0, f0, dh, dl} of each column
     float rho2c[NCOL];
+    float dz[BK];             // zc - s3 of the brick's voxel layers under this view
     int count[NCOL];          // cuts per column (before the G-phase: nonzero flag)
     float vox[NCOL * MUS];    // forward: mu; backward: accumulators
     float* img;               // this view's image (forward: output, backward: input)
@@ -340,6 +342,12 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             s.img = FWD ? p.proj_out + vl * npx : const_cast<float*>(p.proj_in) + vl * npx;
             s.scale = p.scales + size_t(vc.scale_slot) * npx;
         };
+        if (!FWD && tid >= NT - BK) {
+            // per-layer dz of this view (threads outside the G-phase)
+            const int kk = tid - (NT - BK);
+            const double zc64 = sc.minz + (k0 + kk + 0.5) * sc.a3;
+            s.dz[kk] = EXACT ? float(zc64 - vc.s3) : float(zc64) - float(vc.s3);
+        }
         if (tid < NCOL) {
             const int c = tid;
             const int i = i0 + (c % BI), j = j0 + (c / BI);
@@ -410,8 +418,12 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 const int kk = lane + 32 * (hf0 + t);
                 const int k = k0 + kk;
                 v.kvalid = k < k1;
-                const double zc64 = sc.minz + (k + 0.5) * sc.a3;
-                v.dz = EXACT ? float(zc64 - vc.s3) : float(zc64) - float(vc.s3);
+                if (FWD) {  // (the shared copy costs the forward spills)
+                    const double zc64 = sc.minz + (k + 0.5) * sc.a3;
+                    v.dz = EXACT ? float(zc64 - vc.s3) : float(zc64) - float(vc.s3);
+                } else {
+                    v.dz = lds_f32(sbase + uint32_t(offsetof(Smem, dz)) + 4u * kk);
+                }
                 v.dz2e28 = v.dz * v.dz * 1e28f;  // rho2 < dz2e28  <=>  dz^2 > 1e-28 rho2
                 v.vaddr = sbase + uint32_t(offsetof(Smem, vox)) + 4u * (c * MUS + kk);
                 v.mu = FWD ? lds_f32(v.vaddr) : 0.f;
