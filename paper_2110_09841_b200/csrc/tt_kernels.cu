@@ -63,7 +63,15 @@ struct TTSmem {
     float2 amp[NCOL];         // {l_phi0, 1/(u0^2 + f^2)}
     float vox[NCOL * MUS];
     int tile_m0, tile_n0, tile_rows, tile_cols, tile_stride, tile_ok;
+    float mu_abs_max;         // forward: max |mu| over the brick
+    float qscale;             // forward: fixed-point scale of this (brick, view)
 };
+
+__device__ __forceinline__ void red_s32(int* a, int v) {
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(a))),
+                 "r"(v)
+                 : "memory");
+}
 
 __device__ __forceinline__ float frcp(float x) {
     float y;
@@ -205,6 +213,9 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
     const int vg1 = min(vg0 + p.views_per_group, p.view_begin + p.view_count);
     if (vg0 >= vg1) return;
     const size_t plane = size_t(sc.n1) * sc.n2;
+    if (tid == 0) s.mu_abs_max = 0.f;
+    __syncthreads();
+    float abs_max = 0.f;
     for (int idx = tid; idx < NCOL * BK; idx += NT) {
         const int kk = idx / NCOL, c = idx % NCOL;
         const int i = i0 + (c % BI), j = j0 + (c / BI), k = k0 + kk;
@@ -212,7 +223,13 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
         if (FWD && i < i1 && j < j1 && k < k1)
             val = __ldg(p.vol_in + size_t(k) * plane + size_t(j) * sc.n1 + i);
         s.vox[c * MUS + kk] = val;
+        abs_max = fmaxf(abs_max, fabsf(val));
     }
+    if (FWD) {
+        for (int o = 16; o > 0; o >>= 1) abs_max = fmaxf(abs_max, __shfl_xor_sync(0xffffffffu, abs_max, o));
+        if (lane == 0) atomicMax(reinterpret_cast<int*>(&s.mu_abs_max), __float_as_int(abs_max));
+    }
+    int* itile = reinterpret_cast<int*>(tile);  // forward: fixed-point accumulators
     const int rows = sc.rows, cols = sc.cols;
     const size_t npx = size_t(rows) * cols;
     for (int v = vg0; v < vg1; ++v) {
@@ -239,6 +256,7 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
             if (tid == NCOL) {
                 // footprint rectangle of the brick (corner projections)
                 double cmin = INFINITY, cmax = -INFINITY, rmin = INFINITY, rmax = -INFINITY;
+                double dn = INFINITY, df = -INFINITY, zmax = 0.0;
                 for (int q = 0; q < 8; ++q) {
                     const double x = sc.minx + ((q & 1) ? i1 : i0) * sc.a1 - vc.sx;
                     const double y = sc.miny + ((q & 2) ? j1 : j0) * sc.a2 - vc.sy;
@@ -249,6 +267,24 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
                     cmax = fmax(cmax, c1);
                     rmin = fmin(rmin, c2);
                     rmax = fmax(rmax, c2);
+                    dn = fmin(dn, d);
+                    df = fmax(df, d);
+                    zmax = fmax(zmax, fabs(z));
+                }
+                if (FWD) {
+                    // Fixed-point scale: bound on any pixel's partial sum from
+                    // this brick, sum_j mu_j a_j F1_j(n) F2_j(m):
+                    //   a_j <= diag_xy * sqrt(1 + (v_max b2 / f)^2) (A1/A2 amplitude);
+                    //   sum over columns of F1(n) <= BI + BJ (a ray crosses at most
+                    //     BI + BJ cells of the brick's base grid; unit-height trapezoids);
+                    //   sum over layers of F2(m) <= W/delta + 1 (trapezoid support
+                    //     over the layer spacing, both in rows).
+                    const double diag = sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2);
+                    const double vmax = fmax(vc.pp2, double(rows - 1) - vc.pp2) + 1.0;
+                    const double amax = diag * sqrt(1.0 + vmax * vmax * vc.b2 * vc.b2 / (vc.f * vc.f));
+                    const double wd = (df / dn) * (1.0 + 2.0 * zmax * (df - dn) / (df * sc.a3));
+                    const double bound = double(s.mu_abs_max) * amax * double(BI + BJ) * (wd + 2.0) * 1.05;
+                    s.qscale = (bound > 0.0 && dn > 0.0) ? float(1073741824.0 / bound) : 0.f;
                 }
                 const int n0 = max(int(ceil(cmin - 0.5)) - 1, 0), n1 = min(int(floor(cmax + 0.5)) + 1, cols - 1);
                 const int m0 = max(int(ceil(rmin - 0.5)) - 1, 0), m1 = min(int(floor(rmax + 0.5)) + 1, rows - 1);
@@ -265,7 +301,7 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
                 const int tm0 = s.tile_m0, tn0 = s.tile_n0, trows = s.tile_rows, tcols = s.tile_cols;
                 const int tstride = s.tile_stride;
                 if (FWD) {
-                    for (int idx = tid - NCOL; idx < tstride * tcols; idx += NT - NCOL) tile[idx] = 0.f;
+                    for (int idx = tid - NCOL; idx < tstride * tcols; idx += NT - NCOL) itile[idx] = 0;
                 } else {
                     const float* img = p.proj_in + vloc * npx;
                     for (int idx = tid - NCOL; idx < trows * tcols; idx += NT - NCOL) {
@@ -321,6 +357,7 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
             const float ampA1 = amp.x * sqrtf(1.f + (u - pm) * (u - pm) * b2 * b2 * amp.y);
             float acc = 0.f;
             const bool active = kvalid && (!FWD || mu != 0.f);
+            const float muq = FWD ? mu * s.qscale : 0.f;  // fixed-point scale folded into mu
             // the whole (rows x columns) footprint of this voxel inside the tile?
             const bool inside = tile_ok && mf >= tm0 && ml < tm0 + trows && nfirst >= tn0 &&
                                 nfirst + ncache <= tn0 + tcols;
@@ -340,13 +377,13 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
                     }
                     const float wrow = a * f2;
                     if (inside) {
-                        float* trow = tile + (nfirst - tn0) * tstride + (m - tm0);
+                        const int off = (nfirst - tn0) * tstride + (m - tm0);
                         for (int q = 0; q < ncache; ++q) {
                             const float w = wrow * s.f1[q * NCOL + c];
                             if (FWD)
-                                atomicAdd(trow + q * tstride, mu * w);
+                                red_s32(itile + off + q * tstride, __float2int_rn(muq * w));
                             else
-                                acc = fmaf(w, trow[q * tstride], acc);
+                                acc = fmaf(w, tile[off + q * tstride], acc);
                         }
                     } else {
                         for (int q = 0; q < ncache; ++q) {
@@ -357,7 +394,7 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
                                                  unsigned(cc) < unsigned(tcols);
                             if (FWD) {
                                 if (in_tile)
-                                    atomicAdd(&tile[cc * tstride + r], mu * w);
+                                    red_s32(itile + cc * tstride + r, __float2int_rn(muq * w));
                                 else
                                     atomicAdd(out_img + size_t(m) * cols + n, mu * w);
                             } else {
@@ -396,10 +433,11 @@ __global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
         }
         if (FWD && tile_ok) {
             __syncthreads();
+            const float inv_qs = s.qscale > 0.f ? 1.f / s.qscale : 0.f;
             for (int idx = tid; idx < trows * tcols; idx += NT) {
                 const int r = idx / tcols, cc = idx % tcols;
-                const float val = tile[cc * tstride + r];
-                if (val != 0.f) atomicAdd(out_img + size_t(tm0 + r) * cols + (tn0 + cc), val);
+                const int q = itile[cc * tstride + r];
+                if (q != 0) atomicAdd(out_img + size_t(tm0 + r) * cols + (tn0 + cc), float(q) * inv_qs);
             }
         }
     }
