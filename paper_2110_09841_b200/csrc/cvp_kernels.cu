@@ -66,6 +66,10 @@ static_assert(NH % NV == 0, "whole voxel groups per column");
 #endif
 #define CVP_SPLIT_FWD_OK(fwd) (CVP_SPLIT_FWD || !(fwd))
 
+#ifndef CVP_FLUSH_ZERO
+#define CVP_FLUSH_ZERO 1
+#endif
+
 // Per-lane state of one voxel in the V-phase.
 struct VoxState {
     int Mi;
@@ -261,6 +265,10 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
     // Stage the brick's voxels: [column][k] with odd stride (bank-conflict free).
     if (tid < NCOL) s.count[tid] = 0;
     if (tid == 0) s.mu_abs_max = 0.f;
+    // forward: the fixed-point tile starts zeroed and every flush re-zeroes
+    // the pixels it reads, so views need no zeroing pass of their own
+    if (FWD && CVP_FLUSH_ZERO)
+        for (int idx = tid; idx < p.tile_cap; idx += NT) itile[idx] = 0;
     __syncthreads();
     float abs_max = 0.f;
     for (int idx = tid; idx < NCOL * BK; idx += NT) {
@@ -295,7 +303,8 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             const int tm0 = s.tile_m0, tn0 = s.tile_n0, trows = s.tile_rows, tcols = s.tile_cols;
             const int tstride = s.tile_stride;
             if (FWD) {
-                for (int idx = t0; idx < tstride * tcols; idx += step) itile[idx] = 0;
+                if (!CVP_FLUSH_ZERO)
+                    for (int idx = t0; idx < tstride * tcols; idx += step) itile[idx] = 0;
             } else {
                 const float* img = s.img;
                 const float* scale = s.scale;
@@ -383,7 +392,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
         // the brick's footprint misses the detector in this view: every
         // record would be clamped away (cvp.cpp:183-201), nothing to do
         if (trows == 0 || tcols == 0) continue;
-        if (!SPLIT && tile_ok) {
+        if (!SPLIT && tile_ok && !(FWD && CVP_FLUSH_ZERO)) {
             tile_prologue(tid, NT);
             __syncthreads();
         }
@@ -527,6 +536,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 const int r = idx / tcols, cc = idx % tcols;
                 const int q = itile[cc * tstride + r];
                 if (q != 0) {
+                    if (CVP_FLUSH_ZERO) itile[cc * tstride + r] = 0;
                     const size_t px = size_t(tm0 + r) * cols + (tn0 + cc);
                     atomicAdd(s.img + px, float(q) * inv_qs);
                 }
