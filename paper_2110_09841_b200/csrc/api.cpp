@@ -286,7 +286,8 @@ int device_error(cvpb_context* ctx, cudaStream_t st) {
 
 int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_policy* exec,
             bool forward, const float* vol_in, float* vol_out, const float* proj_in,
-            float* proj_out, int view_begin, int view_count, int accumulate, cudaStream_t st) {
+            float* proj_out, int view_begin, int view_count, int accumulate, cudaStream_t st,
+            const double* vol_in64 = nullptr, double* vol_out64 = nullptr) {
     CVPB_TRY(check_ctx(ctx));
     CVPB_TRY(check_cvp_options(opts));
     CVPB_TRY(check_range(ctx, view_begin, view_count));
@@ -311,6 +312,9 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     L.deterministic = exec ? exec->deterministic : 0;
     L.tile_need = ctx->cvp_tile_need;
     L.tall_voxels = ctx->voxel_rows > 1.4 ? 1 : 0;
+    L.vol_in64 = vol_in64;
+    L.vol_copy = vol_in64 ? const_cast<float*>(vol_in) : nullptr;
+    L.vol_out64 = vol_out64;
     L.err = ctx->d_err.p;
     if (!forward && view_count == 0 && !accumulate) {
         CVPB_CUDA(cudaMemsetAsync(vol_out, 0, sizeof(float) * ctx->nvox(), st));
@@ -364,6 +368,21 @@ int ensure_host_buffers(cvpb_context* ctx) {
         CVPB_CUDA(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
     }
     return CVPB_OK;
+}
+
+// Device pointer of a caller's page-locked (pinned / registered) host buffer,
+// or null for pageable memory. The host path reads / writes pinned float64
+// volumes in place from the kernels (zero-copy, overlapped with the
+// projector) instead of staging them through a bulk copy.
+template <class T>
+T* mapped_host(T* host) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+    return static_cast<T*>(a.devicePointer);
 }
 
 // View chunks of the host path: [begin, end) of chunk c out of n.
@@ -728,8 +747,14 @@ int cvpb_project_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
     const size_t nv = ctx->nvox(), npx = ctx->npx_view();
     const int nviews = int(ctx->views.size());
     CVPB_CUDA(cudaEventRecord(ctx->ev0, st));
-    CVPB_CUDA(cudaMemcpyAsync(ctx->d_stage.p, volume, sizeof(double) * nv, cudaMemcpyHostToDevice, st));
-    CVPB_CUDA(cvpb::launch_f64_to_f32(ctx->d_stage.p, ctx->h_vol.p, nv, st));
+    // pinned input: the first chunk's bricks read it in place and leave a
+    // float32 device copy for the later chunks (pageable input: one bulk
+    // copy first)
+    const double* vol_map = mapped_host(volume);
+    if (!vol_map) {
+        CVPB_CUDA(cudaMemcpyAsync(ctx->d_stage.p, volume, sizeof(double) * nv, cudaMemcpyHostToDevice, st));
+        CVPB_CUDA(cvpb::launch_f64_to_f32(ctx->d_stage.p, ctx->h_vol.p, nv, st));
+    }
     // view chunks: chunk c's projections go back to the host (float64) on the
     // copy stream while chunk c + 1 is projected
     const int n = host_chunks(nviews);
@@ -737,7 +762,7 @@ int cvpb_project_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
         const int v0 = chunk_begin(nviews, n, c), v1 = chunk_begin(nviews, n, c + 1);
         const size_t off = npx * size_t(v0), cnt = npx * size_t(v1 - v0);
         CVPB_TRY(run_cvp(ctx, opts, exec, true, ctx->h_vol.p, nullptr, nullptr, ctx->h_proj.p + off,
-                         v0, v1 - v0, 0, st));
+                         v0, v1 - v0, 0, st, c == 0 ? vol_map : nullptr));
         CVPB_CUDA(cudaEventRecord(ctx->ev_chunk[c], st));
         CVPB_CUDA(cudaStreamWaitEvent(cs, ctx->ev_chunk[c], 0));
         CVPB_CUDA(cvpb::launch_f32_to_f64(ctx->h_proj.p + off, ctx->d_stage.p + off, cnt, cs));
@@ -778,14 +803,19 @@ int cvpb_backproject_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
         CVPB_CUDA(cvpb::launch_f64_to_f32(ctx->d_stage.p + off, ctx->h_proj.p + off, cnt, cs));
         CVPB_CUDA(cudaEventRecord(ctx->ev_chunk[c], cs));
     }
+    // pinned output: the last chunk's bricks write the float64 result in place
+    double* vol_map = mapped_host(volume);
     for (int c = 0; c < n; ++c) {
         const int v0 = chunk_begin(nviews, n, c), v1 = chunk_begin(nviews, n, c + 1);
         CVPB_CUDA(cudaStreamWaitEvent(st, ctx->ev_chunk[c], 0));
         CVPB_TRY(run_cvp(ctx, opts, exec, false, nullptr, ctx->h_vol.p,
-                         ctx->h_proj.p + npx * size_t(v0), nullptr, v0, v1 - v0, c > 0 ? 1 : 0, st));
+                         ctx->h_proj.p + npx * size_t(v0), nullptr, v0, v1 - v0, c > 0 ? 1 : 0, st,
+                         nullptr, c == n - 1 ? vol_map : nullptr));
     }
-    CVPB_CUDA(cvpb::launch_f32_to_f64(ctx->h_vol.p, ctx->d_stage.p, nv, st));
-    CVPB_CUDA(cudaMemcpyAsync(volume, ctx->d_stage.p, sizeof(double) * nv, cudaMemcpyDeviceToHost, st));
+    if (!vol_map) {
+        CVPB_CUDA(cvpb::launch_f32_to_f64(ctx->h_vol.p, ctx->d_stage.p, nv, st));
+        CVPB_CUDA(cudaMemcpyAsync(volume, ctx->d_stage.p, sizeof(double) * nv, cudaMemcpyDeviceToHost, st));
+    }
     CVPB_CUDA(cudaEventRecord(ctx->ev1, st));
     CVPB_TRY(device_error(ctx, st));
     if (view_seconds) {

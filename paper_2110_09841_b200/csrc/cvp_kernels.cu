@@ -86,6 +86,9 @@ struct CvpParams {
     const float* scales;      // [slots][rows*cols]
     const float* vol_in;      // forward input
     float* vol_out;           // backward output
+    const double* vol_in64;   // forward input, mapped host float64 (instead of vol_in)
+    float* vol_copy;          // with vol_in64: float32 copy of the input left here
+    double* vol_out64;        // backward output, mapped host float64 (instead of vol_out)
     const float* proj_in;     // backward input (view_begin-relative)
     float* proj_out;          // forward output (view_begin-relative)
     int view_begin, view_count, views_per_group;
@@ -276,7 +279,13 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
         const int i = i0 + (c % BI), j = j0 + (c / BI), k = k0 + kk;
         float val = 0.f;
         if (FWD && i < i1 && j < j1 && k < k1) {
-            val = __ldg(p.vol_in + size_t(k) * plane + size_t(j) * sc.n1 + i);
+            const size_t off = size_t(k) * plane + size_t(j) * sc.n1 + i;
+            if (p.vol_in64) {
+                val = float(p.vol_in64[off]);
+                if (p.vol_copy) p.vol_copy[off] = val;
+            } else {
+                val = __ldg(p.vol_in + off);
+            }
             if (val != 0.f) s.count[c] = 1;
             abs_max = fmaxf(abs_max, fabsf(val));
         }
@@ -549,14 +558,18 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             const int kk = idx / NCOL, c = idx % NCOL;
             const int i = i0 + (c % BI), j = j0 + (c / BI), kq = k0 + kk;
             if (i < i1 && j < j1 && kq < k1) {
-                float* dst = p.vol_out + size_t(kq) * plane + size_t(j) * sc.n1 + i;
+                const size_t off = size_t(kq) * plane + size_t(j) * sc.n1 + i;
+                float* dst = p.vol_out + off;
                 const float val = s.vox[c * MUS + kk];
-                if (p.atomic_out)
+                if (p.atomic_out) {
                     atomicAdd(dst, val);
-                else if (p.accumulate)
-                    *dst += val;
-                else
-                    *dst = val;
+                } else {
+                    const float out = p.accumulate ? *dst + val : val;
+                    if (p.vol_out64)
+                        p.vol_out64[off] = double(out);
+                    else
+                        *dst = out;
+                }
             }
         }
     }
@@ -776,6 +789,9 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
     p.scales = L.scales;
     p.vol_in = L.vol_in;
     p.vol_out = L.vol_out;
+    p.vol_in64 = L.vol_in64;
+    p.vol_copy = L.vol_copy;
+    p.vol_out64 = groups > 1 ? nullptr : L.vol_out64;  // atomic view groups: convert after
     p.proj_in = L.proj_in;
     p.proj_out = L.proj_out;
     p.view_begin = L.view_begin;
@@ -808,8 +824,10 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
                                                                        L.view_begin, npx);
         return cudaGetLastError();
     }
-    return L.exact ? launch_opts<true, false>(p, grid, dyn, L.tall_voxels, stream)
-                   : launch_opts<false, false>(p, grid, dyn, L.tall_voxels, stream);
+    e = L.exact ? launch_opts<true, false>(p, grid, dyn, L.tall_voxels, stream)
+                : launch_opts<false, false>(p, grid, dyn, L.tall_voxels, stream);
+    if (e != cudaSuccess || !L.vol_out64 || p.vol_out64) return e;
+    return launch_f32_to_f64(L.vol_out, L.vol_out64, size_t(sc.n1) * sc.n2 * sc.n3, stream);
 }
 
 cudaError_t launch_scale_image(double f, double pp1, double pp2, double b1, double b2, int rows,

@@ -21,6 +21,12 @@ struct CvpLaunch {
     int accumulate, deterministic;
     int tile_need;            // largest brick footprint (floats), see launch_cvp_tile_need
     int tall_voxels;          // voxels ~2 detector rows tall: three straight-line rows
+    // host-path zero-copy (mapped pinned float64 host buffers, device pointers):
+    // forward reads the volume straight from the host while staging bricks;
+    // backward writes its (accumulated) result straight to the host
+    const double* vol_in64 = nullptr;
+    float* vol_copy = nullptr;  // forward with vol_in64: also leave a float32 copy here
+    double* vol_out64 = nullptr;
     int* err;                 // device error flag
 };
 

@@ -96,6 +96,18 @@ def test_carm_fine_pixels_exact_beats_reference_single(checker):
     assert max_rel(bp, bp_ref) <= EXACT_MAX, max_rel(bp, bp_ref)
 
 
+def test_c2_geometry_tall_voxels_exact(checker):
+    """configs[1] geometry (0.18 mm voxels, 0.154 mm C-arm pixels, SID 749 /
+    SDD 1198): voxels ~1.9 detector rows tall, so the launch takes the
+    three-straight-line-row walk; exact parity with the reference Double."""
+    p, p_ref, bp, bp_ref, scene = _run_pair(checker, (96, 96, 96), (0.18, 0.18, 0.18), 480, 616,
+                                            0.154, 0.154, 749.0, 1198.0, 4, (1, 1, 0, 1), arc=200.0)
+    assert rel_l2(p, p_ref) <= EXACT_L2 and max_rel(p, p_ref) <= EXACT_MAX, (
+        rel_l2(p, p_ref), max_rel(p, p_ref))
+    assert rel_l2(bp, bp_ref) <= EXACT_L2 and max_rel(bp, bp_ref) <= EXACT_MAX, (
+        rel_l2(bp, bp_ref), max_rel(bp, bp_ref))
+
+
 def test_large_cone_angle_exact(checker):
     """configs[3]-style short SID/SDD (300/500), 1 mm pixels, 0.5 mm voxels."""
     p, p_ref, bp, bp_ref, _ = _run_pair(checker, (48, 48, 48), (0.5, 0.5, 0.5), 128, 128, 1.0, 1.0,
@@ -215,6 +227,32 @@ def test_host_path_view_chunks_match_device_path():
     b_host = cb.backproject_cvp(p_host, views, geom)
     b_dev = _np(scene.backproject_cvp(scene.project_cvp(_torch_vol(x64, geom))))
     assert rel_l2(b_host.values, b_dev) < 1e-6
+
+
+@pytest.mark.parametrize("n_views", [5, 37])
+def test_host_path_pinned_buffers_match_pageable(n_views):
+    # pinned float64 host buffers take the zero-copy route (the forward
+    # stages bricks straight from the host volume, the backward's last view
+    # chunk writes the float64 result in place); same results up to the
+    # float atomic merge order of view groups (small scenes)
+    import torch
+    import paper_2110_09841_b200 as cb
+    geom, det, views, _ = make_case((24, 20, 28), (1.0, 1.0, 1.0), 40, 36, 1.0, 1.0, 60.0, 100.0,
+                                    n_views)
+    scene = cb.DeviceScene(geom, det, views)
+    x64 = cb.fill_uniform01(geom.voxel_count(), 13)
+    b64 = cb.fill_uniform01(det.pixel_count() * n_views, 14)
+    xp = torch.from_numpy(x64).pin_memory()
+    bp = torch.from_numpy(b64).pin_memory()
+    pp = torch.zeros(det.pixel_count() * n_views, dtype=torch.float64).pin_memory()
+    vp = torch.zeros(geom.voxel_count(), dtype=torch.float64).pin_memory()
+    for _ in range(2):  # the second pass reuses the context's host-path buffers
+        scene.project_cvp_host(xp.numpy(), pp.numpy())
+        scene.backproject_cvp_host(bp.numpy(), vp.numpy())
+        p_ref = scene.project_cvp_host(np.array(x64))
+        v_ref = scene.backproject_cvp_host(np.array(b64))
+        assert rel_l2(pp.numpy(), p_ref) < 1e-6
+        assert rel_l2(vp.numpy(), v_ref) < 1e-6
 
 
 def test_scale_images_match_reference(reference):
