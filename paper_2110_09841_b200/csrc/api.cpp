@@ -212,6 +212,7 @@ struct cvpb_context {
     DevBuf<float> d_scale_cos, d_scale_exact;
     DevBuf<int> d_err, d_box, d_flag;
     DevBuf<double> d_partials, d_stage;
+    DevBuf<unsigned char> d_cut_table;  // CVP per-(view, column) cut table scratch
     DevBuf<float> h_vol, h_proj;  // device buffers of the host path
     DevBuf<float> cg_r, cg_q, cg_s, cg_p;
     DevBuf<int> d_rec_i;
@@ -284,6 +285,28 @@ int device_error(cvpb_context* ctx, cudaStream_t st) {
     return fail(CVPB_DOMAIN_ERROR, "centroid of a degenerate polygon");
 }
 
+// Scratch for the CVP cut table of up to `view_count` views: the whole range
+// when it fits (c3: 512^2 columns x 496 views = 18.7 GB), else the largest
+// view chunk within a third of the free device memory (launch_cvp then splits
+// the launch into view chunks).
+int reserve_cut_table(cvpb_context* ctx, int view_count, void*& mem, size_t& bytes) {
+    const size_t per_view = size_t(ctx->sc.n1) * ctx->sc.n2 * cvpb::kCutTableBytes;
+    size_t want = per_view * size_t(std::max(view_count, 1));
+    if (ctx->d_cut_table.n < want) {
+        size_t free_b = 0, total_b = 0;
+        CVPB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const size_t cap = (free_b + ctx->d_cut_table.n) / 3;
+        if (want > cap) want = std::max(per_view, cap / per_view * per_view);
+        if (ctx->d_cut_table.n < want) {
+            ctx->d_cut_table.release();
+            CVPB_CUDA(ctx->d_cut_table.reserve(want));
+        }
+    }
+    mem = ctx->d_cut_table.p;
+    bytes = ctx->d_cut_table.n;
+    return CVPB_OK;
+}
+
 int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_policy* exec,
             bool forward, const float* vol_in, float* vol_out, const float* proj_in,
             float* proj_out, int view_begin, int view_count, int accumulate, cudaStream_t st,
@@ -312,6 +335,7 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     L.deterministic = exec ? exec->deterministic : 0;
     L.tile_need = ctx->cvp_tile_need;
     L.tall_voxels = ctx->voxel_rows > 1.4 ? 1 : 0;
+    CVPB_TRY(reserve_cut_table(ctx, view_count, L.cut_table, L.cut_table_bytes));
     L.vol_in64 = vol_in64;
     L.vol_copy = vol_in64 ? const_cast<float*>(vol_in) : nullptr;
     L.vol_out64 = vol_out64;
@@ -464,6 +488,7 @@ void cvpb_context_destroy(cvpb_context* ctx) {
     ctx->d_flag.release();
     ctx->d_partials.release();
     ctx->d_stage.release();
+    ctx->d_cut_table.release();
     ctx->d_rec_i.release();
     ctx->d_rec_d.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);

@@ -80,8 +80,23 @@ struct VoxState {
 constexpr int MAXC = 4;                 // cuts cached per column; more are recomputed
 constexpr int MUS = BK + 1;             // padded column stride of the voxel tile
 
+// Column cuts of every voxel column under views [v0, v0 + nv), computed once
+// per (view, column) by cut_table_kernel instead of once per brick: the
+// G-phase of a brick becomes a load. Index (v - v0) * ncols + j * n1 + i;
+// cut slot q of a column at ((v - v0) * MAXC + q) * ncols + column.
+struct CutTable {
+    int* count;
+    double* Q0;
+    float* rho2c;
+    float4* cutA;  // {A, g, rho2, shw}
+    float4* cutB;  // {kc, tr_a, tr_b, n (bits)}
+    int v0, nv;
+    int ncols;
+};
+
 struct CvpParams {
     Scene sc;
+    CutTable t;
     const ViewConst* views;
     const float* scales;      // [slots][rows*cols]
     const float* vol_in;      // forward input
@@ -252,11 +267,14 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
     const Scene& sc = p.sc;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nbi = (sc.n1 + BI - 1) / BI, nbj = (sc.n2 + BJ - 1) / BJ;
+    // k fastest: the bricks of one column stack run together and share the
+    // cut-table reads in L2
+    const int nbk = (sc.n3 + BK - 1) / BK;
     int b = blockIdx.x;
+    const int bk = b % nbk;
+    b /= nbk;
     const int bi = b % nbi;
-    b /= nbi;
-    const int bj = b % nbj;
-    const int bk = b / nbj;
+    const int bj = b / nbi;
     const int i0 = bi * BI, j0 = bj * BJ, k0 = bk * BK;
     const int i1 = min(i0 + BI, sc.n1), j1 = min(j0 + BJ, sc.n2), k1 = min(k0 + BK, sc.n3);
 
@@ -371,20 +389,22 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             const int i = i0 + (c % BI), j = j0 + (c / BI);
             int cnt = 0;
             if (i < i1 && j < j1 && (!FWD || s.count[c])) {
-                ColumnRec col;
-                cnt = column_cuts<EXACT>(vc, sc, i, j, true, corr, col, [&](const CutRec& r) {
-                    if (cnt < MAXC) store_cut(s, cnt * NCOL + c, r);
-                    ++cnt;
-                });
-                if (cnt < 0) {
-                    atomicOr(p.err, kDevSourcePlane);
-                    cnt = 0;
+                // the column's cuts from the table (cut_table_kernel)
+                const size_t col = size_t(j) * sc.n1 + i;
+                const size_t vl = size_t(v - p.t.v0);
+                const size_t base = vl * p.t.ncols + col;
+                cnt = __ldg(p.t.count + base);
+                const int nc = min(cnt, MAXC);
+                for (int q = 0; q < nc; ++q) {
+                    const size_t slot = (vl * MAXC + q) * p.t.ncols + col;
+                    s.cutA[q * NCOL + c] = __ldg(p.t.cutA + slot);
+                    s.cutB[q * NCOL + c] = __ldg(p.t.cutB + slot);
                 }
                 const ColumnAnchor an = column_anchor<EXACT>(
-                    vc.pp2, sc.minz + (k0 + 0.5) * sc.a3 - vc.s3, col.Q0, sc.a3);
+                    vc.pp2, sc.minz + (k0 + 0.5) * sc.a3 - vc.s3, __ldg(p.t.Q0 + base), sc.a3);
                 s.anchor[c] = make_int4(an.M0, __float_as_int(an.f0), __float_as_int(an.dh),
                                         __float_as_int(an.dl));
-                s.rho2c[c] = col.rho2c;
+                s.rho2c[c] = __ldg(p.t.rho2c + base);
             }
             s.count[c] = cnt;
         } else if (SPLIT) {
@@ -724,6 +744,57 @@ cudaError_t launch_opts(const CvpParams& p, dim3 grid, int dyn, bool tall, cudaS
                        : launch_variant<EXACT, FWD, false, false, 2>(p, grid, dyn, stream);
 }
 
+// The per-(view, column) cut table (BandCutter + compute_cuts + fill_cut_info,
+// cvp.cpp:73-157, via column_cuts): one thread per (view, column), consecutive
+// threads on consecutive columns so the SoA stores coalesce.
+template <bool EXACT>
+__global__ void cut_table_kernel(Scene sc, const ViewConst* views, CutTable t, int corr, int* err) {
+    const size_t ncols = size_t(t.ncols);
+    const size_t total = ncols * t.nv;
+    for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += size_t(gridDim.x) * blockDim.x) {
+        const size_t col = idx % ncols, vl = idx / ncols;
+        const int i = int(col % sc.n1), j = int(col / sc.n1);
+        ColumnRec rec;
+        int cnt = 0;
+        cnt = column_cuts<EXACT>(views[t.v0 + vl], sc, i, j, true, corr != 0, rec, [&](const CutRec& r) {
+            if (cnt < MAXC) {
+                const size_t slot = (vl * MAXC + cnt) * ncols + col;
+                t.cutA[slot] = make_float4(r.A, r.g, r.rho2, r.shw);
+                t.cutB[slot] = make_float4(r.kc, r.tr_a, r.tr_b, __int_as_float(r.n));
+            }
+            ++cnt;
+        });
+        if (cnt < 0) {
+            atomicOr(err, kDevSourcePlane);
+            cnt = 0;
+        }
+        t.count[idx] = cnt;
+        t.Q0[idx] = rec.Q0;
+        t.rho2c[idx] = rec.rho2c;
+    }
+}
+
+// Carve a cut table for nv views out of the scratch block.
+CutTable cut_table_layout(void* mem, int ncols, int v0, int nv) {
+    CutTable t;
+    const size_t n = size_t(ncols) * nv;
+    unsigned char* m = static_cast<unsigned char*>(mem);
+    t.cutA = reinterpret_cast<float4*>(m);
+    m += sizeof(float4) * n * MAXC;
+    t.cutB = reinterpret_cast<float4*>(m);
+    m += sizeof(float4) * n * MAXC;
+    t.Q0 = reinterpret_cast<double*>(m);
+    m += sizeof(double) * n;
+    t.count = reinterpret_cast<int*>(m);
+    m += sizeof(int) * n;
+    t.rho2c = reinterpret_cast<float*>(m);
+    t.v0 = v0;
+    t.nv = nv;
+    t.ncols = ncols;
+    return t;
+}
+
 // Largest tile (odd row stride x columns) any brick needs under any view.
 __global__ void tile_need_kernel(Scene sc, const ViewConst* views, int n_views, int* need) {
     const int nbi = (sc.n1 + BI - 1) / BI, nbj = (sc.n2 + BJ - 1) / BJ, nbk = (sc.n3 + BK - 1) / BK;
@@ -774,60 +845,90 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
     if (tile_cap <= fit3) tile_cap = fit3;
     const int dyn = int(sizeof(Smem)) + tile_cap * int(sizeof(float));
     const int nbricks = ((sc.n1 + BI - 1) / BI) * ((sc.n2 + BJ - 1) / BJ) * ((sc.n3 + BK - 1) / BK);
-    // Enough CTAs to fill 148 SMs x 2 resident: split views into groups when
-    // the volume has few bricks (c1: 32 bricks). Deterministic mode keeps one
-    // group so the backward accumulation order is fixed.
-    int groups = 1;
-    const int target = 148 * 2 * 2;
-    if (!L.deterministic && nbricks < target) groups = std::min(L.view_count, (target + nbricks - 1) / nbricks);
-    const int per = (L.view_count + groups - 1) / groups;
-    groups = (L.view_count + per - 1) / per;
 
     CvpParams p;
     p.sc = sc;
     p.views = L.views;
     p.scales = L.scales;
-    p.vol_in = L.vol_in;
-    p.vol_out = L.vol_out;
-    p.vol_in64 = L.vol_in64;
-    p.vol_copy = L.vol_copy;
-    p.vol_out64 = groups > 1 ? nullptr : L.vol_out64;  // atomic view groups: convert after
-    p.proj_in = L.proj_in;
-    p.proj_out = L.proj_out;
-    p.view_begin = L.view_begin;
-    p.view_count = L.view_count;
-    p.views_per_group = per;
     p.corr = L.elevation_correction;
     p.per_row_r = L.cut_centroid;
     p.h = float(0.5 * sc.a3);
     p.tile_cap = tile_cap;
-    p.accumulate = L.accumulate;
-    p.atomic_out = groups > 1 ? 1 : 0;
     p.err = L.err;
 
+    // view chunks whose cut table fits the scratch block
+    const int ncols = sc.n1 * sc.n2;
+    const size_t per_view = size_t(ncols) * kCutTableBytes;
+    const int chunk = int(std::min<size_t>(size_t(L.view_count), L.cut_table ? L.cut_table_bytes / per_view : 0));
+    if (chunk < 1) return cudaErrorMemoryAllocation;
+    static_assert(kCutTableBytes == 2 * MAXC * sizeof(float4) + sizeof(double) + sizeof(int) + sizeof(float),
+                  "cut table layout");
+    const size_t npx = size_t(sc.rows) * sc.cols;
+    const size_t nvox = size_t(sc.n1) * sc.n2 * sc.n3;
+
     cudaError_t e;
-    if (!L.forward && groups > 1 && !L.accumulate) {
-        e = cudaMemsetAsync(L.vol_out, 0, sizeof(float) * size_t(sc.n1) * sc.n2 * sc.n3, stream);
+    if (L.forward) {
+        e = cudaMemsetAsync(L.proj_out, 0, sizeof(float) * npx * L.view_count, stream);
         if (e != cudaSuccess) return e;
     }
-    dim3 grid(nbricks, groups);
+    for (int c0 = 0; c0 < L.view_count; c0 += chunk) {
+        const int cn = std::min(chunk, L.view_count - c0);
+        const int cv0 = L.view_begin + c0;
+        const bool first = c0 == 0, last = c0 + cn == L.view_count;
+        p.t = cut_table_layout(L.cut_table, ncols, cv0, cn);
+        {
+            const size_t total = size_t(ncols) * cn;
+            const int blocks = int(std::min<size_t>((total + 255) / 256, 148 * 64));
+            if (L.exact)
+                cut_table_kernel<true><<<blocks, 256, 0, stream>>>(sc, L.views, p.t, L.elevation_correction, L.err);
+            else
+                cut_table_kernel<false><<<blocks, 256, 0, stream>>>(sc, L.views, p.t, L.elevation_correction, L.err);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+        }
+        // Enough CTAs to fill 148 SMs x 2 resident: split views into groups
+        // when the volume has few bricks (c1: 32 bricks). Deterministic mode
+        // keeps one group so the backward accumulation order is fixed.
+        int groups = 1;
+        const int target = 148 * 2 * 2;
+        if (!L.deterministic && nbricks < target) groups = std::min(cn, (target + nbricks - 1) / nbricks);
+        const int per = (cn + groups - 1) / groups;
+        groups = (cn + per - 1) / per;
+        p.view_begin = cv0;
+        p.view_count = cn;
+        p.views_per_group = per;
+        p.vol_in = L.vol_in;
+        p.vol_out = L.vol_out;
+        p.vol_in64 = first ? L.vol_in64 : nullptr;   // later chunks read the float32 copy
+        p.vol_copy = first ? L.vol_copy : nullptr;
+        p.proj_in = L.proj_in ? L.proj_in + size_t(c0) * npx : nullptr;
+        p.proj_out = L.proj_out ? L.proj_out + size_t(c0) * npx : nullptr;
+        p.accumulate = first ? L.accumulate : 1;
+        p.atomic_out = groups > 1 ? 1 : 0;
+        // zero-copy float64 output on the last chunk (atomic view groups: convert after)
+        p.vol_out64 = (last && groups == 1) ? L.vol_out64 : nullptr;
+        if (!L.forward && groups > 1 && !p.accumulate) {
+            e = cudaMemsetAsync(L.vol_out, 0, sizeof(float) * nvox, stream);
+            if (e != cudaSuccess) return e;
+        }
+        dim3 grid(nbricks, groups);
+        e = L.forward ? (L.exact ? launch_opts<true, true>(p, grid, dyn, L.tall_voxels, stream)
+                                 : launch_opts<false, true>(p, grid, dyn, L.tall_voxels, stream))
+                      : (L.exact ? launch_opts<true, false>(p, grid, dyn, L.tall_voxels, stream)
+                                 : launch_opts<false, false>(p, grid, dyn, L.tall_voxels, stream));
+        if (e != cudaSuccess) return e;
+        if (!L.forward && last && L.vol_out64 && !p.vol_out64) {
+            e = launch_f32_to_f64(L.vol_out, L.vol_out64, nvox, stream);
+            if (e != cudaSuccess) return e;
+        }
+    }
     if (L.forward) {
-        e = cudaMemsetAsync(L.proj_out, 0, sizeof(float) * size_t(sc.rows) * sc.cols * L.view_count,
-                            stream);
-        if (e != cudaSuccess) return e;
-        e = L.exact ? launch_opts<true, true>(p, grid, dyn, L.tall_voxels, stream)
-                    : launch_opts<false, true>(p, grid, dyn, L.tall_voxels, stream);
-        if (e != cudaSuccess) return e;
-        const size_t npx = size_t(sc.rows) * sc.cols;
         const int bx = int(std::min<size_t>((npx + 255) / 256, 64));
         apply_scale_kernel<<<dim3(bx, L.view_count), 256, 0, stream>>>(L.proj_out, L.scales, L.views,
                                                                        L.view_begin, npx);
         return cudaGetLastError();
     }
-    e = L.exact ? launch_opts<true, false>(p, grid, dyn, L.tall_voxels, stream)
-                : launch_opts<false, false>(p, grid, dyn, L.tall_voxels, stream);
-    if (e != cudaSuccess || !L.vol_out64 || p.vol_out64) return e;
-    return launch_f32_to_f64(L.vol_out, L.vol_out64, size_t(sc.n1) * sc.n2 * sc.n3, stream);
+    return cudaSuccess;
 }
 
 cudaError_t launch_scale_image(double f, double pp1, double pp2, double b1, double b2, int rows,

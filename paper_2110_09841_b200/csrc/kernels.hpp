@@ -24,6 +24,10 @@ struct CvpLaunch {
     // host-path zero-copy (mapped pinned float64 host buffers, device pointers):
     // forward reads the volume straight from the host while staging bricks;
     // backward writes its (accumulated) result straight to the host
+    // scratch for the per-(view, column) cut table (kCutTableBytes per
+    // column-view); launches are split into view chunks that fit
+    void* cut_table = nullptr;
+    size_t cut_table_bytes = 0;
     const double* vol_in64 = nullptr;
     float* vol_copy = nullptr;  // forward with vol_in64: also leave a float32 copy here
     double* vol_out64 = nullptr;
@@ -33,6 +37,8 @@ struct CvpLaunch {
 cudaError_t launch_cvp_tile_need(const Scene& sc, const ViewConst* views, int n_views, int* d_need,
                                  cudaStream_t stream);
 cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream);
+// bytes of cut table per (view, voxel column): count, Q0, rho2c, 4 x 2 float4
+constexpr size_t kCutTableBytes = 4 + 8 + 4 + 4 * 32;
 cudaError_t launch_scale_image(double f, double pp1, double pp2, double b1, double b2, int rows,
                                int cols, int exact, float* out, double* out64, cudaStream_t stream);
 cudaError_t launch_cut_records(const Scene& sc, const ViewConst* views, int view, int i, int j,
