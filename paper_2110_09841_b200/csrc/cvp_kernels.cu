@@ -77,7 +77,7 @@ struct VoxState {
     uint32_t vaddr;
     bool kvalid, active;
 };
-constexpr int MAXC = 4;                 // cuts cached per column; more are recomputed
+constexpr int MAXC = kCutSlots;         // cuts cached per column; more are recomputed
 constexpr int MUS = BK + 1;             // padded column stride of the voxel tile
 
 // Column cuts of every voxel column under views [v0, v0 + nv), computed once

@@ -37,8 +37,12 @@ struct CvpLaunch {
 cudaError_t launch_cvp_tile_need(const Scene& sc, const ViewConst* views, int n_views, int* d_need,
                                  cudaStream_t stream);
 cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream);
-// bytes of cut table per (view, voxel column): count, Q0, rho2c, 4 x 2 float4
-constexpr size_t kCutTableBytes = 4 + 8 + 4 + 4 * 32;
+// bytes of cut table per (view, voxel column): count, Q0, rho2c, MAXC x 2 float4
+#ifndef CVP_MAXC
+#define CVP_MAXC 4
+#endif
+constexpr int kCutSlots = CVP_MAXC;
+constexpr size_t kCutTableBytes = 4 + 8 + 4 + kCutSlots * 32;
 cudaError_t launch_scale_image(double f, double pp1, double pp2, double b1, double b2, int rows,
                                int cols, int exact, float* out, double* out64, cudaStream_t stream);
 cudaError_t launch_cut_records(const Scene& sc, const ViewConst* views, int view, int i, int j,
