@@ -295,7 +295,10 @@ int reserve_cut_table(cvpb_context* ctx, int view_count, void*& mem, size_t& byt
     if (ctx->d_cut_table.n < want) {
         size_t free_b = 0, total_b = 0;
         CVPB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        const size_t cap = (free_b + ctx->d_cut_table.n) / 3;
+        size_t cap = (free_b + ctx->d_cut_table.n) / 3;
+        // CVPB_CUT_TABLE_MAX_BYTES caps it further (tests force view chunks)
+        if (const char* env = std::getenv("CVPB_CUT_TABLE_MAX_BYTES"))
+            cap = std::min(cap, size_t(std::strtoull(env, nullptr, 10)));
         if (want > cap) want = std::max(per_view, cap / per_view * per_view);
         if (ctx->d_cut_table.n < want) {
             ctx->d_cut_table.release();

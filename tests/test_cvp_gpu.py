@@ -280,3 +280,22 @@ def test_view_chunks_and_accumulate_compose():
     p_full = scene.project_cvp(full)
     p_part = scene.project_cvp(full, view_begin=3, view_count=5)
     assert rel_l2(_np(p_part), _np(p_full)[3:8]) < 1e-6
+
+
+def test_cut_table_view_chunks_match_single_chunk(checker, monkeypatch):
+    """A cut table too small for the launch splits it into view chunks (c5
+    at full size takes two); chunked P / BP match the reference and the
+    single-chunk launch."""
+    import paper_2110_09841_b200 as cb
+    counts, nv = (24, 20, 28), 37
+    per_view = counts[0] * counts[1] * 144
+    p1, p_ref, b1, b_ref, _ = _run_pair(checker, counts, (1.0, 1.0, 1.0), 40, 36, 1.0, 1.0, 60.0,
+                                        100.0, nv, (1, 1, 0, 1))
+    monkeypatch.setenv("CVPB_CUT_TABLE_MAX_BYTES", str(5 * per_view))  # 8 chunks of <= 5 views
+    p8, _, b8, _, _ = _run_pair(checker, counts, (1.0, 1.0, 1.0), 40, 36, 1.0, 1.0, 60.0, 100.0,
+                                nv, (1, 1, 0, 1))
+    for got in (p1, p8):
+        assert rel_l2(got, p_ref) <= EXACT_L2 and max_rel(got, p_ref) <= EXACT_MAX
+    for got in (b1, b8):
+        assert rel_l2(got, b_ref) <= EXACT_L2 and max_rel(got, b_ref) <= EXACT_MAX
+    assert rel_l2(p8, p1) < 1e-6 and rel_l2(b8, b1) < 1e-6
