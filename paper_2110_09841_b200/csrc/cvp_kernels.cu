@@ -69,6 +69,9 @@ static_assert(NH % NV == 0, "whole voxel groups per column");
 #ifndef CVP_FLUSH_ZERO
 #define CVP_FLUSH_ZERO 1
 #endif
+#ifndef CVP_DZ_SMEM_FWD
+#define CVP_DZ_SMEM_FWD 1  // per-layer dz staged in shared memory for the forward too
+#endif
 
 // Per-lane state of one voxel in the V-phase.
 struct VoxState {
@@ -378,8 +381,9 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             s.img = FWD ? p.proj_out + vl * npx : const_cast<float*>(p.proj_in) + vl * npx;
             s.scale = p.scales + size_t(vc.scale_slot) * npx;
         };
-        if (!FWD && tid >= NT - BK) {
-            // per-layer dz of this view (threads outside the G-phase)
+        if ((!FWD || CVP_DZ_SMEM_FWD) && tid >= NT - BK) {
+            // per-layer dz of this view (threads outside the G-phase; no
+            // float64 per voxel-column in the V-phase)
             const int kk = tid - (NT - BK);
             const double zc64 = sc.minz + (k0 + kk + 0.5) * sc.a3;
             s.dz[kk] = EXACT ? float(zc64 - vc.s3) : float(zc64) - float(vc.s3);
@@ -456,7 +460,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 const int kk = lane + 32 * (hf0 + t);
                 const int k = k0 + kk;
                 v.kvalid = k < k1;
-                if (FWD) {  // (the shared copy costs the forward spills)
+                if (FWD && !CVP_DZ_SMEM_FWD) {
                     const double zc64 = sc.minz + (k + 0.5) * sc.a3;
                     v.dz = EXACT ? float(zc64 - vc.s3) : float(zc64) - float(vc.s3);
                 } else {
