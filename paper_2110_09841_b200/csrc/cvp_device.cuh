@@ -350,13 +350,10 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
         m_last = min(m_last, rows - 1);
         e = fmaxf(e, -Mf);
     }
-#ifndef CVP_DENSE_NORET
-#define CVP_DENSE_NORET 1
-#endif
     // DENSE: an empty range (voxel off the detector rows) emits zero weights
     // instead of branching out
     const bool nonempty = m_first <= m_last;
-    if (!(DENSE && CVP_DENSE_NORET) && !nonempty) return;
+    if (!DENSE && !nonempty) return;
     // spread of the elevation rectangle at boundary e: |beta(e)| halfw with
     // beta(e) = (b2/f) hw (pm - e)  (cvp.cpp:205)
     const float dtop = pmh - e;
@@ -367,14 +364,8 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
     // voxel's own corners): T = h exactly. The branch is warp-uniform in
     // practice, so the clamp-mean runs only for the rare straddling lane.
     const float s_top = sh * fabsf(dtop);
-#ifndef CVP_TTOP_FREE
-#define CVP_TTOP_FREE 0
-#endif
     float t_top = h;
-    if (CVP_TTOP_FREE)
-        t_top = clamp_mean_local(a_top, s_top, h);
-    else if (a_top - s_top < h)
-        t_top = clamp_mean_local(a_top, s_top, h);
+    if (a_top - s_top < h) t_top = clamp_mean_local(a_top, s_top, h);
     int m = m_first;
     if (DENSE) {
         // Rows 1 and 2 in straight-line code (a voxel-cut spans 1-2 rows in
@@ -404,7 +395,7 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
         }
         const float2 WI = mul2(make_float2(fmaxf(W.x, 0.f), fmaxf(W.y, 0.f)), inv);
         const bool two = m_last > m_first;
-        emit(m_first, CVP_DENSE_NORET && !nonempty ? 0.f : WI.x);
+        emit(m_first, nonempty ? WI.x : 0.f);
         emit(m_first + 1, two ? WI.y : 0.f);  // may lie past m_last (and the detector): weight 0
         if constexpr (NR >= 3) {
             // third row (boundary e + 3) in straight-line code as well

@@ -3,23 +3,31 @@
 // Reference: /root/reference/proj/src/cvp.cpp forward_view (:357-412),
 // backward_view (:414-458), project/backproject_cvp_impl (:460-500).
 //
-// Work decomposition: one CTA owns a brick of
-// BI x BJ voxel columns x BK voxels along x3 and loops over its views.
-// Per view:
-//   G-phase  one thread per column computes that column's cuts (float64 in
-//            exact mode) into shared memory; warp 0 computes the brick's
-//            detector footprint rectangle;
-//   V-phase  warp w walks columns w, w+8, ...; lane = voxel k in the brick;
-//            each (voxel, cut, row) record is
-//              forward:  atomically added into a shared-memory detector tile
-//                        (column-major, conflict-free for consecutive rows),
-//              backward: gathered from a shared-memory copy of the scaled
-//                        image footprint (no atomics);
-//   flush    forward: the tile is added to HBM with one coalesced float atomic
-//            per touched pixel, multiplied by the phase-2 pixel scale
-//            (cvp.cpp:473-474) on the way out.
+// Work decomposition:
+//   cut table  cut_table_kernel computes the column cuts of every voxel column
+//              once per view (float64 world quantities in exact mode);
+//   bricks     one CTA owns BI x BJ voxel columns x BK voxels along x3
+//              (8 x 16 x 64, bricks numbered k-fastest) and loops over views:
+//   G-phase    one thread per column loads its cuts from the table into
+//              shared memory and splits its chi2 anchor; the other warps bound
+//              the brick's detector footprint and (backward) stage the tile;
+//   V-phase    warp w walks columns w, w+8, ...; each lane carries the voxels
+//              k = lane and lane + 32 through every cut, and each
+//              (voxel, cut, row) record is
+//                forward:  added (int32 fixed point) into a shared-memory
+//                          detector tile (column-major, odd stride),
+//                backward: gathered from a shared-memory copy of the scaled
+//                          image footprint (no atomics);
+//   flush      forward: the tile is added to HBM with one float atomic per
+//              touched pixel and re-zeroed; the phase-2 pixel scale
+//              (cvp.cpp:473-474) is one streaming pass after the launch.
 // The brick's attenuation values (forward) / accumulators (backward) stay in
 // shared memory across all views, so HBM sees the volume once per launch.
+//
+// Build parameters (defaults are the measured optimum on B200, see
+// profiles/ncu_r01.md): CVP_BI / CVP_BJ / CVP_BK brick shape, CVP_NV voxels
+// per lane per cut pass, CVP_NT threads, CVP_MINB resident CTAs per SM,
+// CVP_MAXC (kernels.hpp) cut slots per column.
 #include <algorithm>
 #include <cstddef>
 #include <cstdio>
@@ -60,18 +68,6 @@ static_assert(NT - BK >= NCOL, "per-layer dz threads lie outside the G-phase");
 #endif
 constexpr int NV = CVP_NV;              // voxels per lane per cut pass (kk = lane + 32 t)
 static_assert(NH % NV == 0, "whole voxel groups per column");
-
-#ifndef CVP_SPLIT_FWD
-#define CVP_SPLIT_FWD 0
-#endif
-#define CVP_SPLIT_FWD_OK(fwd) (CVP_SPLIT_FWD || !(fwd))
-
-#ifndef CVP_FLUSH_ZERO
-#define CVP_FLUSH_ZERO 1
-#endif
-#ifndef CVP_DZ_SMEM_FWD
-#define CVP_DZ_SMEM_FWD 1  // per-layer dz staged in shared memory for the forward too
-#endif
 
 // Per-lane state of one voxel in the V-phase.
 struct VoxState {
@@ -291,7 +287,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
     if (tid == 0) s.mu_abs_max = 0.f;
     // forward: the fixed-point tile starts zeroed and every flush re-zeroes
     // the pixels it reads, so views need no zeroing pass of their own
-    if (FWD && CVP_FLUSH_ZERO)
+    if (FWD)
         for (int idx = tid; idx < p.tile_cap; idx += NT) itile[idx] = 0;
     __syncthreads();
     float abs_max = 0.f;
@@ -326,29 +322,26 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
     for (int v = vg0; v < vg1; ++v) {
         const ViewConst& vc = p.views[v];
         __syncthreads();  // previous view's V-phase / flush is complete
-        // ---- tile prologue: forward zeroes the fixed-point tile, backward
-        // stages the scaled image footprint (threads t0, t0 + step, ...) ----
+        // ---- backward tile prologue: stage the scaled image footprint
+        // (threads t0, t0 + step, ...) ----------------------------------------
         auto tile_prologue = [&](int t0, int step) {
             if (!s.tile_ok || s.tile_rows == 0 || s.tile_cols == 0) return;
             const int tm0 = s.tile_m0, tn0 = s.tile_n0, trows = s.tile_rows, tcols = s.tile_cols;
             const int tstride = s.tile_stride;
-            if (FWD) {
-                if (!CVP_FLUSH_ZERO)
-                    for (int idx = t0; idx < tstride * tcols; idx += step) itile[idx] = 0;
-            } else {
-                const float* img = s.img;
-                const float* scale = s.scale;
-                for (int idx = t0; idx < trows * tcols; idx += step) {
-                    const int r = idx / tcols, cc = idx % tcols;
-                    const size_t px = size_t(tm0 + r) * cols + (tn0 + cc);
-                    tile[cc * tstride + r] = __ldg(img + px) * __ldg(scale + px);
-                }
+            const float* img = s.img;
+            const float* scale = s.scale;
+            for (int idx = t0; idx < trows * tcols; idx += step) {
+                const int r = idx / tcols, cc = idx % tcols;
+                const size_t px = size_t(tm0 + r) * cols + (tn0 + cc);
+                tile[cc * tstride + r] = __ldg(img + px) * __ldg(scale + px);
             }
         };
         // ---- G-phase: column cuts --------------------------------------
         // Warps past the G-phase columns (NCOL < NT) compute the brick
         // footprint and stage the detector tile meanwhile.
-        constexpr bool SPLIT = NCOL < NT && CVP_SPLIT_FWD_OK(FWD);
+        // (backward only: the forward has no prologue — its tile is kept
+        // zeroed by the flush — and moving its footprint work here spills)
+        constexpr bool SPLIT = NCOL < NT && !FWD;
         auto footprint = [&]() {
             int m0, m1, n0, n1;
             double dmin = 0.0, dmax = 0.0;
@@ -381,7 +374,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             s.img = FWD ? p.proj_out + vl * npx : const_cast<float*>(p.proj_in) + vl * npx;
             s.scale = p.scales + size_t(vc.scale_slot) * npx;
         };
-        if ((!FWD || CVP_DZ_SMEM_FWD) && tid >= NT - BK) {
+        if (tid >= NT - BK) {
             // per-layer dz of this view (threads outside the G-phase; no
             // float64 per voxel-column in the V-phase)
             const int kk = tid - (NT - BK);
@@ -425,7 +418,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
         // the brick's footprint misses the detector in this view: every
         // record would be clamped away (cvp.cpp:183-201), nothing to do
         if (trows == 0 || tcols == 0) continue;
-        if (!SPLIT && tile_ok && !(FWD && CVP_FLUSH_ZERO)) {
+        if (!SPLIT && !FWD && tile_ok) {
             tile_prologue(tid, NT);
             __syncthreads();
         }
@@ -438,7 +431,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
         const uint32_t img_slot = sbase + uint32_t(offsetof(Smem, img));
         const uint32_t scale_slot = sbase + uint32_t(offsetof(Smem, scale));
         // Each lane carries NV voxels of one column through every cut (NV = NH
-        // with CVP_PAIR: the cut record, tile test and loop control are shared
+        // = 2: the cut record, tile test and loop control are shared
         // by the lane's voxels kk = lane and lane + 32).
         for (int ch = warp; ch < NCOL * NH / NV; ch += NWARP) {
             constexpr int NG = NH / NV;  // voxel groups per column
@@ -460,12 +453,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 const int kk = lane + 32 * (hf0 + t);
                 const int k = k0 + kk;
                 v.kvalid = k < k1;
-                if (FWD && !CVP_DZ_SMEM_FWD) {
-                    const double zc64 = sc.minz + (k + 0.5) * sc.a3;
-                    v.dz = EXACT ? float(zc64 - vc.s3) : float(zc64) - float(vc.s3);
-                } else {
-                    v.dz = lds_f32(sbase + uint32_t(offsetof(Smem, dz)) + 4u * kk);
-                }
+                v.dz = lds_f32(sbase + uint32_t(offsetof(Smem, dz)) + 4u * kk);
                 v.dz2e28 = v.dz * v.dz * 1e28f;  // rho2 < dz2e28  <=>  dz^2 > 1e-28 rho2
                 v.vaddr = sbase + uint32_t(offsetof(Smem, vox)) + 4u * (c * MUS + kk);
                 v.mu = FWD ? lds_f32(v.vaddr) : 0.f;
@@ -569,7 +557,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 const int r = idx / tcols, cc = idx % tcols;
                 const int q = itile[cc * tstride + r];
                 if (q != 0) {
-                    if (CVP_FLUSH_ZERO) itile[cc * tstride + r] = 0;
+                    itile[cc * tstride + r] = 0;
                     const size_t px = size_t(tm0 + r) * cols + (tn0 + cc);
                     atomicAdd(s.img + px, float(q) * inv_qs);
                 }
