@@ -382,6 +382,18 @@ def main():
                 "kernel": dom, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "note": "4 B/voxel-view (SURVEY 8d); the kernel is issue-bound, see DESIGN.md"}
+    # the bound that binds: instruction issue (ncu smsp__issue_active of the
+    # same kernel, committed capture)
+    issue = None
+    sp = os.path.join(ROOT, "profiles", "ncu_r01_fwd_summary.txt" if pm >= bm else "ncu_r01_bwd_summary.txt")
+    if os.path.exists(sp):
+        with open(sp) as f:
+            for line in f:
+                if "smsp__issue_active.avg.pct_of_peak_sustained_active" in line:
+                    issue = float(line.split()[-1]) / 100.0
+    if issue is not None:
+        roofline["issue"] = {"bound": "issue", "frac": issue, "metric": "smsp__issue_active",
+                             "source": os.path.relpath(sp, ROOT) + " (ncu --set full, 16-view launch)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
