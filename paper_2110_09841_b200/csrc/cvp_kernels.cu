@@ -122,7 +122,8 @@ struct Smem {
     int4 anchor[NCOL];        // ColumnAnchor {M0, f0, dh, dl} of each column
     float rho2c[NCOL];
     float dz[BK];             // zc - s3 of the brick's voxel layers under this view
-    int count[NCOL];          // cuts per column (before the G-phase: nonzero flag)
+    int count[NCOL];          // cuts per column under the current view
+    int nonzero[NCOL];        // forward: the column holds a nonzero attenuation
     float vox[NCOL * MUS];    // forward: mu; backward: accumulators
     float* img;               // this view's image (forward: output, backward: input)
     const float* scale;       // backward: this view's phase-2 factors
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
 
     const size_t plane = size_t(sc.n1) * sc.n2;
     // Stage the brick's voxels: [column][k] with odd stride (bank-conflict free).
-    if (tid < NCOL) s.count[tid] = 0;
+    if (tid < NCOL) s.nonzero[tid] = 0;
     if (tid == 0) s.mu_abs_max = 0.f;
     // forward: the fixed-point tile starts zeroed and every flush re-zeroes
     // the pixels it reads, so views need no zeroing pass of their own
@@ -303,7 +304,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             } else {
                 val = __ldg(p.vol_in + off);
             }
-            if (val != 0.f) s.count[c] = 1;
+            if (val != 0.f) s.nonzero[c] = 1;
             abs_max = fmaxf(abs_max, fabsf(val));
         }
         s.vox[c * MUS + kk] = val;
@@ -385,7 +386,9 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             const int c = tid;
             const int i = i0 + (c % BI), j = j0 + (c / BI);
             int cnt = 0;
-            if (i < i1 && j < j1 && (!FWD || s.count[c])) {
+            // (a separate flag: the per-view cut count may be 0 for a column
+            // whose cuts all fall off the detector in one view only)
+            if (i < i1 && j < j1 && (!FWD || s.nonzero[c])) {
                 // the column's cuts from the table (cut_table_kernel)
                 const size_t col = size_t(j) * sc.n1 + i;
                 const size_t vl = size_t(v - p.t.v0);

@@ -12,7 +12,8 @@ from conftest import max_rel, rel_l2
 pytestmark = pytest.mark.gpu
 
 
-def _case(checker, counts, voxel, rows, cols, pw, ph, views, opts4=(1, 1, 0, 1), x64=None):
+def _case(checker, counts, voxel, rows, cols, pw, ph, views, opts4=(1, 1, 0, 1), x64=None,
+          exec=None):
     import torch
     import paper_2110_09841_b200 as cb
     from oracle.pyoracle import Scene
@@ -28,8 +29,8 @@ def _case(checker, counts, voxel, rows, cols, pw, ph, views, opts4=(1, 1, 0, 1),
                       cb.RadiusEstimate(opts4[3]))
     xt = torch.from_numpy(x64.astype(np.float32)).reshape(geom.shape()).cuda()
     bt = torch.from_numpy(b64.astype(np.float32)).reshape(len(views), rows, cols).cuda()
-    p = scene.project_cvp(xt, opts=o).double().cpu().numpy()
-    bp = scene.backproject_cvp(bt, opts=o).double().cpu().numpy().ravel()
+    p = scene.project_cvp(xt, opts=o, exec=exec).double().cpu().numpy()
+    bp = scene.backproject_cvp(bt, opts=o, exec=exec).double().cpu().numpy().ravel()
     p_ref = checker.project_cvp(sc, x64, opts4)
     bp_ref = checker.backproject_cvp(sc, b64, opts4).ravel()
     return p, p_ref, bp, bp_ref
@@ -69,6 +70,18 @@ def test_volume_wider_than_detector_clamps(checker):
     det = cb.DetectorGeometry.make(24, 20, 1.0, 1.0)
     views = cb.make_circular_trajectory(60.0, 100.0, 6, 360.0, det)
     _assert_close(*_case(checker, (32, 32, 32), (1.0, 1.0, 1.0), 24, 20, 1.0, 1.0, views))
+
+
+def test_views_walked_by_one_brick_with_columns_off_the_detector(checker):
+    """Deterministic mode keeps every view in one CTA (no view groups), as
+    large volumes do: a column whose cuts all fall off the detector in one
+    view must still be projected in the next ones (regression: the per-view
+    cut count once overwrote the forward's nonzero-column flag)."""
+    import paper_2110_09841_b200 as cb
+    det = cb.DetectorGeometry.make(24, 20, 1.0, 1.0)
+    views = cb.make_circular_trajectory(60.0, 100.0, 12, 360.0, det)
+    _assert_close(*_case(checker, (32, 32, 32), (1.0, 1.0, 1.0), 24, 20, 1.0, 1.0, views,
+                         exec=cb.ExecPolicy(deterministic=True)))
 
 
 @pytest.mark.parametrize("opts4", [(1, 1, 0, 1), (0, 0, 0, 0)])

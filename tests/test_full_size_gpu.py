@@ -1,0 +1,61 @@
+"""GPU: the headline configuration at full size (BASELINE configs[2]: 512^3
+@0.09 mm, 616x480 @0.154 mm, SID 749 / SDD 1198) against the reference itself
+on two of the 496 views (the reference takes ~2.5 s per view and direction on
+16 cores), plus the size-independent properties over all 496 views:
+adjointness and linearity of the full-size pair on the device."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import max_rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+N, V = 512, 496
+
+
+def _scene(views_idx=None):
+    import paper_2110_09841_b200 as cb
+    det = cb.DetectorGeometry.make(480, 616, 0.154, 0.154)
+    geom = cb.VolumeGeometry.make((N, N, N), (0.09, 0.09, 0.09))
+    views = cb.make_circular_trajectory(749.0, 1198.0, V, 360.0, det)
+    if views_idx is not None:
+        views = [views[i] for i in views_idx]
+    return cb, geom, det, views
+
+
+def test_full_size_two_views_match_reference(checker):
+    import torch
+    from oracle.pyoracle import Scene
+    idx = [0, 124]  # 0 and 90 degrees
+    cb, geom, det, views = _scene(idx)
+    scene = cb.DeviceScene(geom, det, views)
+    x32 = cb.fill_uniform01(geom.voxel_count(), 7).astype(np.float32)
+    b32 = cb.fill_uniform01(det.pixel_count() * len(idx), 8).astype(np.float32)
+    p = scene.project_cvp(torch.from_numpy(x32).reshape(geom.shape()).cuda()).double().cpu().numpy()
+    bp = scene.backproject_cvp(torch.from_numpy(b32).reshape(len(idx), 480, 616).cuda())
+    bp = bp.double().cpu().numpy().ravel()
+    sc = Scene((N, N, N), (0.09,) * 3, 480, 616, 0.154, 0.154, cb.views_to_array(views))
+    threads = os.cpu_count() or 1
+    p_ref = checker.project_cvp(sc, x32.astype(np.float64), (1, 1, 0, 1), threads=threads)
+    bp_ref = checker.backproject_cvp(sc, b32.astype(np.float64), (1, 1, 0, 1), threads=threads)
+    assert rel_l2(p, p_ref) <= 1e-5 and max_rel(p, p_ref) <= 1e-4, (rel_l2(p, p_ref), max_rel(p, p_ref))
+    assert rel_l2(bp, bp_ref) <= 1e-5 and max_rel(bp, bp_ref) <= 1e-4, (rel_l2(bp, bp_ref),
+                                                                       max_rel(bp, bp_ref))
+
+
+def test_full_size_all_views_adjoint_and_linear():
+    import torch
+    cb, geom, det, views = _scene()
+    scene = cb.DeviceScene(geom, det, views)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.rand(geom.shape(), device="cuda", generator=g)
+    y = torch.rand((V, 480, 616), device="cuda", generator=g)
+    ax = scene.project_cvp(x)
+    aty = scene.backproject_cvp(y)
+    lhs = float(torch.dot(ax.reshape(-1).double(), y.reshape(-1).double()))
+    rhs = float(torch.dot(x.reshape(-1).double(), aty.reshape(-1).double()))
+    assert abs(lhs - rhs) / max(abs(lhs), abs(rhs)) < 1e-5, (lhs, rhs)
+    a2x = scene.project_cvp(2.0 * x)
+    assert float((a2x - 2.0 * ax).norm() / a2x.norm()) < 1e-6
