@@ -141,6 +141,11 @@ int cvpb_pixel_scale(const cvpb_view* view, const cvpb_detector_geometry* det, i
 int cvpb_fill_uniform01(double* out, size_t n, uint64_t seed);
 
 /* ---- CVP (cvp.hpp:81-99) — device buffers ------------------------------- */
+/* Every CVP call first computes the column cuts of its views into a device
+ * cut table owned by the context (144 B per voxel column and view; at most a
+ * third of the free device memory, further capped by the environment variable
+ * CVPB_CUT_TABLE_MAX_BYTES; larger jobs run in view chunks). The table stays
+ * allocated until the context is destroyed. */
 /* project_cvp_into (cvp.cpp:615-626): overwrites views [view_begin,
  * view_begin+view_count) of d_proj (which points at view 0's image of that
  * range, i.e. the caller's slice). */
