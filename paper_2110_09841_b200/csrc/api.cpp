@@ -213,6 +213,14 @@ struct cvpb_context {
     DevBuf<int> d_err, d_box, d_flag;
     DevBuf<double> d_partials, d_stage;
     DevBuf<unsigned char> d_cut_table;  // CVP per-(view, column) cut table scratch
+    // what the table holds (a single-chunk launch's views and options), and
+    // the event after the last launch that read or wrote it: launches on
+    // other streams wait for it, so the shared scratch is stream-ordered
+    struct {
+        int valid = 0, view_begin = 0, view_count = 0, exact = 0, corr = 0;
+    } cut_key;
+    cudaEvent_t ev_table = nullptr;
+    bool ev_table_recorded = false;
     DevBuf<float> h_vol, h_proj;  // device buffers of the host path
     DevBuf<float> cg_r, cg_q, cg_s, cg_p;
     DevBuf<int> d_rec_i;
@@ -338,7 +346,18 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     L.deterministic = exec ? exec->deterministic : 0;
     L.tile_need = ctx->cvp_tile_need;
     L.tall_voxels = ctx->voxel_rows > 1.4 ? 1 : 0;
+    const void* table_before = ctx->d_cut_table.p;
     CVPB_TRY(reserve_cut_table(ctx, view_count, L.cut_table, L.cut_table_bytes));
+    // reuse the resident table (same views and options, e.g. the P and BP of
+    // one CGLS iteration) when the launch runs as one chunk
+    const size_t per_view = size_t(ctx->sc.n1) * ctx->sc.n2 * cvpb::kCutTableBytes;
+    const bool one_chunk = per_view * size_t(view_count) <= L.cut_table_bytes;
+    auto& key = ctx->cut_key;
+    L.cut_table_valid = key.valid && table_before == L.cut_table && key.view_begin == view_begin &&
+                                key.view_count == view_count && key.exact == L.exact &&
+                                key.corr == L.elevation_correction
+                            ? 1
+                            : 0;
     L.vol_in64 = vol_in64;
     L.vol_copy = vol_in64 ? const_cast<float*>(vol_in) : nullptr;
     L.vol_out64 = vol_out64;
@@ -347,7 +366,19 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
         CVPB_CUDA(cudaMemsetAsync(vol_out, 0, sizeof(float) * ctx->nvox(), st));
         return CVPB_OK;
     }
+    if (!ctx->ev_table) CVPB_CUDA(cudaEventCreateWithFlags(&ctx->ev_table, cudaEventDisableTiming));
+    if (ctx->ev_table_recorded) CVPB_CUDA(cudaStreamWaitEvent(st, ctx->ev_table, 0));
+    key.valid = 0;
     CVPB_CUDA(cvpb::launch_cvp(L, st));
+    CVPB_CUDA(cudaEventRecord(ctx->ev_table, st));
+    ctx->ev_table_recorded = true;
+    if (one_chunk && view_count > 0) {
+        key.valid = 1;
+        key.view_begin = view_begin;
+        key.view_count = view_count;
+        key.exact = L.exact;
+        key.corr = L.elevation_correction;
+    }
     return CVPB_OK;
 }
 
@@ -499,6 +530,7 @@ void cvpb_context_destroy(cvpb_context* ctx) {
     for (cudaEvent_t e : ctx->ev_chunk)
         if (e) cudaEventDestroy(e);
     if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
+    if (ctx->ev_table) cudaEventDestroy(ctx->ev_table);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -523,6 +555,7 @@ int cvpb_set_geometry(cvpb_context* ctx, const cvpb_volume_geometry* vol,
     }
     if (n_views < 0) return fail(CVPB_INVALID_ARGUMENT, "negative view count");
     ctx->has_geometry = false;
+    ctx->cut_key.valid = 0;
     ctx->vol = *vol;
     ctx->det = *det;
     ctx->views.assign(views, views + n_views);

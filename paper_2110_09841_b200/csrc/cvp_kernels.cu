@@ -871,7 +871,7 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
         const int cv0 = L.view_begin + c0;
         const bool first = c0 == 0, last = c0 + cn == L.view_count;
         p.t = cut_table_layout(L.cut_table, ncols, cv0, cn);
-        {
+        if (!(L.cut_table_valid && cn == L.view_count)) {
             const size_t total = size_t(ncols) * cn;
             const int blocks = int(std::min<size_t>((total + 255) / 256, 148 * 64));
             if (L.exact)

@@ -28,6 +28,7 @@ struct CvpLaunch {
     // column-view); launches are split into view chunks that fit
     void* cut_table = nullptr;
     size_t cut_table_bytes = 0;
+    int cut_table_valid = 0;  // the table already holds this launch's views (single chunk)
     const double* vol_in64 = nullptr;
     float* vol_copy = nullptr;  // forward with vol_in64: also leave a float32 copy here
     double* vol_out64 = nullptr;

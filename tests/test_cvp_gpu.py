@@ -299,3 +299,34 @@ def test_cut_table_view_chunks_match_single_chunk(checker, monkeypatch):
     for got in (b1, b8):
         assert rel_l2(got, b_ref) <= EXACT_L2 and max_rel(got, b_ref) <= EXACT_MAX
     assert rel_l2(p8, p1) < 1e-6 and rel_l2(b8, b1) < 1e-6
+
+
+def test_cut_table_reuse_follows_options_views_and_streams():
+    """The context keeps the cut table of its last single-chunk launch and
+    reuses it for the same views and options (the P and BP of a CGLS
+    iteration). Switching options or views must recompute it, and launches on
+    different streams are ordered on the shared table."""
+    import torch
+    import paper_2110_09841_b200 as cb
+    geom, det, views, _ = make_case((24, 20, 40), (1.0, 1.0, 1.0), 40, 36, 1.0, 1.0, 60.0, 100.0, 9)
+    x = torch.rand(geom.shape(), device="cuda")
+    y = torch.rand((9, 36, 40), device="cuda")
+    combos = [cb.CvpOptions(), cb.CvpOptions(precision=cb.CvpPrecision.Single),
+              cb.CvpOptions(elevation_correction=False), cb.CvpOptions()]
+    fresh = []
+    for o in combos:
+        sc = cb.DeviceScene(geom, det, views)
+        fresh.append((sc.project_cvp(x, opts=o), sc.backproject_cvp(y, opts=o),
+                      sc.project_cvp(x, opts=o, view_begin=3, view_count=4)))
+    scene = cb.DeviceScene(geom, det, views)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for o, (p_ref, b_ref, ps_ref) in zip(combos, fresh):
+        with torch.cuda.stream(s1):
+            p = scene.project_cvp(x, opts=o, stream=s1)
+        with torch.cuda.stream(s2):
+            b = scene.backproject_cvp(y, opts=o, stream=s2)
+        ps = scene.project_cvp(x, opts=o, view_begin=3, view_count=4)
+        torch.cuda.synchronize()
+        assert rel_l2(p.cpu().numpy(), p_ref.cpu().numpy()) < 1e-6
+        assert rel_l2(b.cpu().numpy(), b_ref.cpu().numpy()) < 1e-6
+        assert rel_l2(ps.cpu().numpy(), ps_ref.cpu().numpy()) < 1e-6
