@@ -348,16 +348,19 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     L.tall_voxels = ctx->voxel_rows > 1.4 ? 1 : 0;
     const void* table_before = ctx->d_cut_table.p;
     CVPB_TRY(reserve_cut_table(ctx, view_count, L.cut_table, L.cut_table_bytes));
-    // reuse the resident table (same views and options, e.g. the P and BP of
-    // one CGLS iteration) when the launch runs as one chunk
+    // reuse the resident table when it covers this launch's views with the
+    // same options (the P and BP of a step or of one CGLS iteration; the
+    // host path's view chunks)
     const size_t per_view = size_t(ctx->sc.n1) * ctx->sc.n2 * cvpb::kCutTableBytes;
     const bool one_chunk = per_view * size_t(view_count) <= L.cut_table_bytes;
     auto& key = ctx->cut_key;
-    L.cut_table_valid = key.valid && table_before == L.cut_table && key.view_begin == view_begin &&
-                                key.view_count == view_count && key.exact == L.exact &&
-                                key.corr == L.elevation_correction
+    L.cut_table_valid = key.valid && table_before == L.cut_table && key.view_begin <= view_begin &&
+                                view_begin + view_count <= key.view_begin + key.view_count &&
+                                key.exact == L.exact && key.corr == L.elevation_correction
                             ? 1
                             : 0;
+    L.table_v0 = key.view_begin;
+    L.table_nv = key.view_count;
     L.vol_in64 = vol_in64;
     L.vol_copy = vol_in64 ? const_cast<float*>(vol_in) : nullptr;
     L.vol_out64 = vol_out64;
@@ -368,17 +371,58 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     }
     if (!ctx->ev_table) CVPB_CUDA(cudaEventCreateWithFlags(&ctx->ev_table, cudaEventDisableTiming));
     if (ctx->ev_table_recorded) CVPB_CUDA(cudaStreamWaitEvent(st, ctx->ev_table, 0));
+    const bool keep = L.cut_table_valid != 0;
     key.valid = 0;
     CVPB_CUDA(cvpb::launch_cvp(L, st));
     CVPB_CUDA(cudaEventRecord(ctx->ev_table, st));
     ctx->ev_table_recorded = true;
-    if (one_chunk && view_count > 0) {
+    if (keep) {
+        key.valid = 1;  // unchanged
+    } else if (one_chunk && view_count > 0) {
         key.valid = 1;
         key.view_begin = view_begin;
         key.view_count = view_count;
         key.exact = L.exact;
         key.corr = L.elevation_correction;
     }
+    return CVPB_OK;
+}
+
+// Cut table of views [view_begin, view_begin + view_count) ahead of several
+// launches over subsets of them (the host path's view chunks); a no-op when
+// it does not fit in one piece (the launches then build their own).
+int prepare_cut_table(cvpb_context* ctx, const cvpb_cvp_options* opts, int view_begin,
+                      int view_count, cudaStream_t st) {
+    CVPB_TRY(check_cvp_options(opts));
+    CVPB_TRY(check_scene_views(ctx));
+    if (ctx->base_reaches_source) return CVPB_OK;  // the launches report it
+    cvpb::CvpLaunch L{};
+    L.sc = ctx->sc;
+    L.views = ctx->d_views.p;
+    L.view_begin = view_begin;
+    L.view_count = view_count;
+    L.exact = opts->precision == CVPB_PRECISION_EXACT ? 1 : 0;
+    L.elevation_correction = opts->elevation_correction ? 1 : 0;
+    L.err = ctx->d_err.p;
+    auto& key = ctx->cut_key;
+    if (key.valid && key.view_begin <= view_begin &&
+        view_begin + view_count <= key.view_begin + key.view_count && key.exact == L.exact &&
+        key.corr == L.elevation_correction)
+        return CVPB_OK;
+    CVPB_TRY(reserve_cut_table(ctx, view_count, L.cut_table, L.cut_table_bytes));
+    const size_t per_view = size_t(ctx->sc.n1) * ctx->sc.n2 * cvpb::kCutTableBytes;
+    if (view_count <= 0 || per_view * size_t(view_count) > L.cut_table_bytes) return CVPB_OK;
+    if (!ctx->ev_table) CVPB_CUDA(cudaEventCreateWithFlags(&ctx->ev_table, cudaEventDisableTiming));
+    if (ctx->ev_table_recorded) CVPB_CUDA(cudaStreamWaitEvent(st, ctx->ev_table, 0));
+    key.valid = 0;
+    CVPB_CUDA(cvpb::launch_cut_table(L, st));
+    CVPB_CUDA(cudaEventRecord(ctx->ev_table, st));
+    ctx->ev_table_recorded = true;
+    key.valid = 1;
+    key.view_begin = view_begin;
+    key.view_count = view_count;
+    key.exact = L.exact;
+    key.corr = L.elevation_correction;
     return CVPB_OK;
 }
 
@@ -817,8 +861,9 @@ int cvpb_project_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
         CVPB_CUDA(cvpb::launch_f64_to_f32(ctx->d_stage.p, ctx->h_vol.p, nv, st));
     }
     // view chunks: chunk c's projections go back to the host (float64) on the
-    // copy stream while chunk c + 1 is projected
+    // copy stream while chunk c + 1 is projected; one cut table serves them all
     const int n = host_chunks(nviews);
+    if (n > 1) CVPB_TRY(prepare_cut_table(ctx, opts, 0, nviews, st));
     for (int c = 0; c < n; ++c) {
         const int v0 = chunk_begin(nviews, n, c), v1 = chunk_begin(nviews, n, c + 1);
         const size_t off = npx * size_t(v0), cnt = npx * size_t(v1 - v0);
@@ -866,6 +911,7 @@ int cvpb_backproject_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
     }
     // pinned output: the last chunk's bricks write the float64 result in place
     double* vol_map = mapped_host(volume);
+    if (n > 1) CVPB_TRY(prepare_cut_table(ctx, opts, 0, nviews, st));
     for (int c = 0; c < n; ++c) {
         const int v0 = chunk_begin(nviews, n, c), v1 = chunk_begin(nviews, n, c + 1);
         CVPB_CUDA(cudaStreamWaitEvent(st, ctx->ev_chunk[c], 0));

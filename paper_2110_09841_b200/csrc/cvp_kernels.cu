@@ -770,6 +770,17 @@ __global__ void cut_table_kernel(Scene sc, const ViewConst* views, CutTable t, i
     }
 }
 
+cudaError_t run_cut_table(const Scene& sc, const ViewConst* views, const CutTable& t, int exact,
+                          int corr, int* err, cudaStream_t stream) {
+    const size_t total = size_t(t.ncols) * t.nv;
+    const int blocks = int(std::min<size_t>((total + 255) / 256, 148 * 64));
+    if (exact)
+        cut_table_kernel<true><<<blocks, 256, 0, stream>>>(sc, views, t, corr, err);
+    else
+        cut_table_kernel<false><<<blocks, 256, 0, stream>>>(sc, views, t, corr, err);
+    return cudaGetLastError();
+}
+
 // Carve a cut table for nv views out of the scratch block.
 CutTable cut_table_layout(void* mem, int ncols, int v0, int nv) {
     CutTable t;
@@ -854,7 +865,11 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
     // view chunks whose cut table fits the scratch block
     const int ncols = sc.n1 * sc.n2;
     const size_t per_view = size_t(ncols) * kCutTableBytes;
-    const int chunk = int(std::min<size_t>(size_t(L.view_count), L.cut_table ? L.cut_table_bytes / per_view : 0));
+    const bool resident = L.cut_table_valid && L.view_begin >= L.table_v0 &&
+                          L.view_begin + L.view_count <= L.table_v0 + L.table_nv;
+    const int chunk = resident ? L.view_count
+                               : int(std::min<size_t>(size_t(L.view_count),
+                                                      L.cut_table ? L.cut_table_bytes / per_view : 0));
     if (chunk < 1) return cudaErrorMemoryAllocation;
     static_assert(kCutTableBytes == 2 * MAXC * sizeof(float4) + sizeof(double) + sizeof(int) + sizeof(float),
                   "cut table layout");
@@ -870,15 +885,11 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
         const int cn = std::min(chunk, L.view_count - c0);
         const int cv0 = L.view_begin + c0;
         const bool first = c0 == 0, last = c0 + cn == L.view_count;
-        p.t = cut_table_layout(L.cut_table, ncols, cv0, cn);
-        if (!(L.cut_table_valid && cn == L.view_count)) {
-            const size_t total = size_t(ncols) * cn;
-            const int blocks = int(std::min<size_t>((total + 255) / 256, 148 * 64));
-            if (L.exact)
-                cut_table_kernel<true><<<blocks, 256, 0, stream>>>(sc, L.views, p.t, L.elevation_correction, L.err);
-            else
-                cut_table_kernel<false><<<blocks, 256, 0, stream>>>(sc, L.views, p.t, L.elevation_correction, L.err);
-            e = cudaGetLastError();
+        if (resident) {
+            p.t = cut_table_layout(L.cut_table, ncols, L.table_v0, L.table_nv);
+        } else {
+            p.t = cut_table_layout(L.cut_table, ncols, cv0, cn);
+            e = run_cut_table(sc, L.views, p.t, L.exact, L.elevation_correction, L.err, stream);
             if (e != cudaSuccess) return e;
         }
         // Enough CTAs to fill 148 SMs x 2 resident: split views into groups
@@ -924,6 +935,15 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
         return cudaGetLastError();
     }
     return cudaSuccess;
+}
+
+cudaError_t launch_cut_table(const CvpLaunch& L, cudaStream_t stream) {
+    const int ncols = L.sc.n1 * L.sc.n2;
+    if (L.view_count <= 0) return cudaSuccess;
+    if (!L.cut_table || size_t(ncols) * kCutTableBytes * L.view_count > L.cut_table_bytes)
+        return cudaErrorMemoryAllocation;
+    return run_cut_table(L.sc, L.views, cut_table_layout(L.cut_table, ncols, L.view_begin, L.view_count),
+                         L.exact, L.elevation_correction, L.err, stream);
 }
 
 cudaError_t launch_scale_image(double f, double pp1, double pp2, double b1, double b2, int rows,

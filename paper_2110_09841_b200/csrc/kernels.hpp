@@ -28,7 +28,8 @@ struct CvpLaunch {
     // column-view); launches are split into view chunks that fit
     void* cut_table = nullptr;
     size_t cut_table_bytes = 0;
-    int cut_table_valid = 0;  // the table already holds this launch's views (single chunk)
+    int cut_table_valid = 0;  // the table already holds views [table_v0, table_v0 + table_nv)
+    int table_v0 = 0, table_nv = 0;  // (valid: a superset of this launch's views, same options)
     const double* vol_in64 = nullptr;
     float* vol_copy = nullptr;  // forward with vol_in64: also leave a float32 copy here
     double* vol_out64 = nullptr;
@@ -38,6 +39,9 @@ struct CvpLaunch {
 cudaError_t launch_cvp_tile_need(const Scene& sc, const ViewConst* views, int n_views, int* d_need,
                                  cudaStream_t stream);
 cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream);
+// Only the cut table of views [L.view_begin, L.view_begin + L.view_count)
+// (must fit L.cut_table_bytes); later launches over subsets reuse it.
+cudaError_t launch_cut_table(const CvpLaunch& L, cudaStream_t stream);
 // bytes of cut table per (view, voxel column): count, Q0, rho2c, MAXC x 2 float4
 #ifndef CVP_MAXC
 #define CVP_MAXC 4
