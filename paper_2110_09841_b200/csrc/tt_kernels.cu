@@ -38,6 +38,9 @@ constexpr int NCOL = BI * BJ;
 constexpr int NT = 256;
 constexpr int NWARP = NT / 32;
 constexpr int NH = BK / 32;   // voxels per lane along x3
+#ifndef TT_MINB
+#define TT_MINB 3             // resident CTAs per SM (80 registers)
+#endif
 static_assert(NCOL < NT, "warps past the columns stage the tile");
 constexpr int MAXN = 6;       // transaxial footprint width cached per column
 constexpr int MUS = BK + 1;
@@ -196,7 +199,7 @@ __device__ WideColumn wide_column(const ViewConst& vc, const Scene& sc, int i, i
 // (named barrier); each lane then carries the voxels kk = lane, lane + 32 of
 // a column through the axial walk.
 template <bool FWD>
-__global__ void __launch_bounds__(NT, 2) tt_brick_kernel(TTParams p) {
+__global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TTSmem& s = *reinterpret_cast<TTSmem*>(smem_raw);
     float* tile = reinterpret_cast<float*>(smem_raw + sizeof(TTSmem));
