@@ -39,7 +39,7 @@ constexpr int NT = 256;
 constexpr int NWARP = NT / 32;
 constexpr int NH = BK / 32;   // voxels per lane along x3
 #ifndef TT_MINB
-#define TT_MINB 3             // resident CTAs per SM (80 registers)
+#define TT_MINB 4             // resident CTAs per SM (64 registers; measured faster than 3 at 80)
 #endif
 static_assert(NCOL < NT, "warps past the columns stage the tile");
 constexpr int MAXN = 6;       // transaxial footprint width cached per column
@@ -463,7 +463,10 @@ __global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
     }
 }
 
-constexpr int kTileCap = 8192;
+// detector tile: what is left of a quarter of the SM's 228 KB of shared
+// memory (four resident CTAs); bricks whose footprint does not fit use the
+// global-memory path
+constexpr int kTileCap = int((228 * 1024 / TT_MINB - 1024 - sizeof(TTSmem)) / sizeof(float));
 
 }  // namespace
 
