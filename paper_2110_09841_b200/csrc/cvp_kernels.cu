@@ -180,11 +180,6 @@ __device__ __forceinline__ uint64_t lds_u64(uint32_t a) {
     return v;
 }
 
-__device__ __forceinline__ void store_cut(Smem& s, int slot, const CutRec& r) {
-    s.cutA[slot] = make_float4(r.A, r.g, r.rho2, r.shw);
-    s.cutB[slot] = make_float4(r.kc, r.tr_a, r.tr_b, __int_as_float(r.n));
-}
-
 __device__ __forceinline__ CutRec load_cut(uint32_t sbase, int slot) {
     const float4 a = lds_f32x4(sbase + uint32_t(offsetof(Smem, cutA)) + 16u * slot);
     const float4 b = lds_f32x4(sbase + uint32_t(offsetof(Smem, cutB)) + 16u * slot);
