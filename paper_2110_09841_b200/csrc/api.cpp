@@ -206,6 +206,10 @@ struct cvpb_context {
     bool base_reaches_source = false;  // (cvp.cpp:82-84), resolved for the whole box
     int n_slots = 0;
     int cvp_tile_need = 0;    // floats, largest brick footprint over the scene
+    int cvp_tile_need_b = 0;  // the same for brick shape B
+    // brick shape per (direction, precision, elevation, radius): 0 = default,
+    // 1 = shape B; chosen by timing both on the scene's first launch
+    std::map<int, int> cvp_shape;
     double r_min = 0.0;       // smallest source-to-volume-box distance over the views
     double voxel_rows = 0.0;  // mean voxel height in detector rows at the volume centre
     DevBuf<ViewConst> d_views;
@@ -220,6 +224,7 @@ struct cvpb_context {
         int valid = 0, view_begin = 0, view_count = 0, exact = 0, corr = 0;
     } cut_key;
     cudaEvent_t ev_table = nullptr;
+    cudaEvent_t ev_tune[2] = {};  // brick-shape timing
     bool ev_table_recorded = false;
     DevBuf<float> h_vol, h_proj;  // device buffers of the host path
     DevBuf<float> cg_r, cg_q, cg_s, cg_p;
@@ -318,6 +323,9 @@ int reserve_cut_table(cvpb_context* ctx, int view_count, void*& mem, size_t& byt
     return CVPB_OK;
 }
 
+int prepare_cut_table(cvpb_context* ctx, const cvpb_cvp_options* opts, int view_begin,
+                      int view_count, cudaStream_t st);
+
 int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_policy* exec,
             bool forward, const float* vol_in, float* vol_out, const float* proj_in,
             float* proj_out, int view_begin, int view_count, int accumulate, cudaStream_t st,
@@ -371,9 +379,51 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     }
     if (!ctx->ev_table) CVPB_CUDA(cudaEventCreateWithFlags(&ctx->ev_table, cudaEventDisableTiming));
     if (ctx->ev_table_recorded) CVPB_CUDA(cudaStreamWaitEvent(st, ctx->ev_table, 0));
+    // brick shape: measured once per scene and option set (both shapes on up
+    // to 24 of this launch's views, written into this launch's own output,
+    // which the real launch then overwrites)
+    // (CVPB_CVP_SHAPE=0 / 1 forces a shape, e.g. for tests)
+    const int shape_key = (L.forward << 3) | (L.exact << 2) | (L.elevation_correction << 1) | L.cut_centroid;
+    auto it = ctx->cvp_shape.find(shape_key);
+    int shape = it != ctx->cvp_shape.end() ? it->second : 0;
+    const char* forced = std::getenv("CVPB_CVP_SHAPE");
+    bool tune = false;
+    if (forced) {
+        shape = std::atoi(forced) == 1 ? 1 : 0;
+    } else if (it == ctx->cvp_shape.end() && view_count >= 8 && (forward || !accumulate) &&
+               !vol_in64 && !vol_out64) {
+        // the timing launches need the whole range's cut table resident
+        if (!L.cut_table_valid) {
+            CVPB_TRY(prepare_cut_table(ctx, opts, view_begin, view_count, st));
+            L.cut_table_valid = key.valid && ctx->d_cut_table.p == L.cut_table ? 1 : 0;
+            L.table_v0 = key.view_begin;
+            L.table_nv = key.view_count;
+        }
+        tune = L.cut_table_valid != 0;
+    }
+    if (tune) {
+        cvpb::CvpLaunch T = L;
+        T.view_count = std::min(view_count, 24);
+        T.accumulate = 0;
+        float ms[2] = {0.f, 0.f};
+        if (!ctx->ev_tune[0])
+            for (cudaEvent_t& e : ctx->ev_tune) CVPB_CUDA(cudaEventCreate(&e));
+        for (int pass = 0; pass < 2; ++pass)  // pass 0 warms both up
+            for (int b = 0; b < 2; ++b) {
+                T.tile_need = b ? ctx->cvp_tile_need_b : ctx->cvp_tile_need;
+                CVPB_CUDA(cudaEventRecord(ctx->ev_tune[0], st));
+                CVPB_CUDA(b ? cvpb::launch_cvp_b(T, st) : cvpb::launch_cvp(T, st));
+                CVPB_CUDA(cudaEventRecord(ctx->ev_tune[1], st));
+                CVPB_CUDA(cudaEventSynchronize(ctx->ev_tune[1]));
+                if (pass) CVPB_CUDA(cudaEventElapsedTime(&ms[b], ctx->ev_tune[0], ctx->ev_tune[1]));
+            }
+        shape = ms[1] < 0.97f * ms[0] ? 1 : 0;  // shape B only for a clear win
+        ctx->cvp_shape[shape_key] = shape;
+    }
+    if (shape) L.tile_need = ctx->cvp_tile_need_b;
     const bool keep = L.cut_table_valid != 0;
     key.valid = 0;
-    CVPB_CUDA(cvpb::launch_cvp(L, st));
+    CVPB_CUDA(shape ? cvpb::launch_cvp_b(L, st) : cvpb::launch_cvp(L, st));
     CVPB_CUDA(cudaEventRecord(ctx->ev_table, st));
     ctx->ev_table_recorded = true;
     if (keep) {
@@ -575,6 +625,8 @@ void cvpb_context_destroy(cvpb_context* ctx) {
         if (e) cudaEventDestroy(e);
     if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
     if (ctx->ev_table) cudaEventDestroy(ctx->ev_table);
+    for (cudaEvent_t e : ctx->ev_tune)
+        if (e) cudaEventDestroy(e);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -672,6 +724,11 @@ int cvpb_set_geometry(cvpb_context* ctx, const cvpb_volume_geometry* vol,
     CVPB_CUDA(cudaMemcpyAsync(&ctx->cvp_tile_need, ctx->d_flag.p, sizeof(int), cudaMemcpyDeviceToHost,
                               ctx->stream));
     CVPB_CUDA(cudaStreamSynchronize(ctx->stream));
+    CVPB_CUDA(cvpb::launch_cvp_tile_need_b(sc, ctx->d_views.p, n_views, ctx->d_flag.p, ctx->stream));
+    CVPB_CUDA(cudaMemcpyAsync(&ctx->cvp_tile_need_b, ctx->d_flag.p, sizeof(int), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    CVPB_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->cvp_shape.clear();
     ctx->has_geometry = true;
     return CVPB_OK;
 }

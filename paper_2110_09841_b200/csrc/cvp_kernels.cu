@@ -36,6 +36,16 @@
 #include "cvp_device.cuh"
 #include "kernels.hpp"
 
+// The file is compiled twice (Makefile): the default brick shape, and shape
+// B (CVP_CFG_B: 8x8x64 at four CTAs per SM, faster on some scenes); the
+// brick-dependent entry points of the second copy carry a _b suffix and
+// the shape-independent ones exist once.
+#ifdef CVP_CFG_B
+#define CVP_PUB(name) name##_b
+#else
+#define CVP_PUB(name) name
+#endif
+
 namespace cvpb {
 
 namespace {
@@ -821,8 +831,8 @@ __global__ void tile_need_kernel(Scene sc, const ViewConst* views, int n_views, 
 
 }  // namespace
 
-cudaError_t launch_cvp_tile_need(const Scene& sc, const ViewConst* views, int n_views, int* d_need,
-                                 cudaStream_t stream) {
+cudaError_t CVP_PUB(launch_cvp_tile_need)(const Scene& sc, const ViewConst* views, int n_views,
+                                          int* d_need, cudaStream_t stream) {
     cudaError_t e = cudaMemsetAsync(d_need, 0, sizeof(int), stream);
     if (e != cudaSuccess || n_views <= 0) return e;
     tile_need_kernel<<<148 * 4, 256, 0, stream>>>(sc, views, n_views, d_need);
@@ -836,7 +846,7 @@ constexpr int kSmemBudget3 = (228 * 1024) / CVP_MINB - 1024;
 constexpr int kTileCapMax = 16384;
 }  // namespace
 
-cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
+cudaError_t CVP_PUB(launch_cvp)(const CvpLaunch& L, cudaStream_t stream) {
     const Scene& sc = L.sc;
     if (L.view_count <= 0) return cudaSuccess;
     // size the detector tile to the scene's largest brick footprint; three
@@ -932,6 +942,7 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream) {
     return cudaSuccess;
 }
 
+#ifndef CVP_CFG_B
 cudaError_t launch_cut_table(const CvpLaunch& L, cudaStream_t stream) {
     const int ncols = L.sc.n1 * L.sc.n2;
     if (L.view_count <= 0) return cudaSuccess;
@@ -961,5 +972,6 @@ cudaError_t launch_cut_records(const Scene& sc, const ViewConst* views, int view
                                                        clamp, cap, rows, cols, vol, inv, n_out, err);
     return cudaGetLastError();
 }
+#endif  // !CVP_CFG_B
 
 }  // namespace cvpb

@@ -118,3 +118,20 @@ def test_view_subrange_equals_slice(checker):
     assert float((part - full[4:7]).norm() / full[4:7].norm()) < 1e-6
     empty = scene.project_cvp(x, view_begin=2, view_count=0)
     assert empty.shape[0] == 0
+
+
+@pytest.mark.parametrize("shape", ["0", "1"])
+def test_both_brick_shapes_match_reference(checker, monkeypatch, shape):
+    """The library carries two brick shapes (8x16x64 at three CTAs per SM and
+    8x8x64 at four) and times both on a scene's first launches; each must
+    match the reference on its own (CVPB_CVP_SHAPE forces one)."""
+    import paper_2110_09841_b200 as cb
+    monkeypatch.setenv("CVPB_CVP_SHAPE", shape)
+    det = cb.DetectorGeometry.make(40, 52, 1.0, 1.0)
+    views = cb.make_circular_trajectory(70.0, 120.0, 9, 360.0, det)
+    _assert_close(*_case(checker, (30, 36, 70), (0.8, 0.8, 0.8), 40, 52, 1.0, 1.0, views,
+                         exec=cb.ExecPolicy(deterministic=True)))
+    det = cb.DetectorGeometry.make(96, 128, 0.154, 0.154)
+    views = cb.make_circular_trajectory(749.0, 1198.0, 8, 360.0, det)
+    _assert_close(*_case(checker, (40, 40, 40), (0.09, 0.09, 0.09), 96, 128, 0.154, 0.154, views,
+                         opts4=(0, 1, 0, 0)))
