@@ -1,0 +1,52 @@
+"""GPU: randomized parity against the reference — random lattices, voxel and
+pixel aspect ratios, detector sizes, source distances, arcs, view counts,
+options, execution modes and brick shapes (tools/random_parity.py runs the
+same generator at larger counts; profiles/random_parity_r01.md)."""
+import numpy as np
+import pytest
+
+from conftest import max_rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_geometry_exact_parity(checker, monkeypatch, seed):
+    import torch
+    import paper_2110_09841_b200 as cb
+    from oracle.pyoracle import Scene
+    rng = np.random.default_rng(1000 + seed)
+    counts = tuple(int(x) for x in rng.integers(5, 48, 3))
+    vox = tuple(float(x) for x in rng.uniform(0.2, 1.5, 3))
+    rows, cols = (int(x) for x in rng.integers(16, 120, 2))
+    pw, ph = (float(x) for x in rng.uniform(0.3, 1.6, 2))
+    ext = float(np.linalg.norm(np.array(counts) * np.array(vox)))
+    sid = float(rng.uniform(0.6, 3.0) * ext + 5.0)
+    sdd = float(sid * rng.uniform(1.2, 2.5))
+    nv = int(rng.integers(1, 24))
+    arc = float(rng.choice([360.0, 200.0, 90.0]))
+    opts4 = (int(rng.integers(0, 2)), int(rng.integers(0, 2)), 0, int(rng.integers(0, 2)))
+    ex = cb.ExecPolicy(deterministic=bool(rng.integers(0, 2)))
+    monkeypatch.setenv("CVPB_CVP_SHAPE", str(int(rng.integers(0, 2))))
+    det = cb.DetectorGeometry.make(rows, cols, pw, ph)
+    geom = cb.VolumeGeometry.make(counts, vox)
+    views = cb.make_circular_trajectory(sid, sdd, nv, arc, det)
+    sc = Scene(counts, vox, rows, cols, pw, ph, cb.views_to_array(views))
+    x = cb.fill_uniform01(geom.voxel_count(), 100 + seed).astype(np.float32).astype(np.float64)
+    if seed % 3 == 0:
+        x[rng.random(x.size) < 0.9] = 0.0
+    b = cb.fill_uniform01(det.pixel_count() * nv, 200 + seed).astype(np.float32).astype(np.float64)
+    scene = cb.DeviceScene(geom, det, views)
+    o = cb.CvpOptions(cb.PixelScaling(opts4[0]), bool(opts4[1]), cb.CvpPrecision(0),
+                      cb.RadiusEstimate(opts4[3]))
+    p = scene.project_cvp(torch.from_numpy(x.astype(np.float32)).reshape(geom.shape()).cuda(), opts=o,
+                          exec=ex).double().cpu().numpy()
+    bp = scene.backproject_cvp(torch.from_numpy(b.astype(np.float32)).reshape(nv, rows, cols).cuda(),
+                               opts=o, exec=ex).double().cpu().numpy()
+    p_ref = checker.project_cvp(sc, x, opts4)
+    bp_ref = checker.backproject_cvp(sc, b, opts4)
+    if np.abs(p_ref).max() > 0:
+        assert rel_l2(p, p_ref) <= 1e-5 and max_rel(p, p_ref) <= 1e-4, (rel_l2(p, p_ref), max_rel(p, p_ref))
+    else:
+        assert np.abs(p).max() == 0
+    assert rel_l2(bp, bp_ref) <= 1e-5 and max_rel(bp, bp_ref) <= 1e-4, (rel_l2(bp, bp_ref), max_rel(bp, bp_ref))
