@@ -1,3 +1,5 @@
+"""CGLS ms/iteration on the c3 scene (device-resident cvpb_cgls), before and
+after a host-path call: (T(3) - T(1)) / 2 after a warm-up call."""
 import sys, time, numpy as np, torch
 sys.path.insert(0, ".")
 import paper_2110_09841_b200 as cb

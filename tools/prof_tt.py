@@ -1,3 +1,4 @@
+"""Profiling driver for the TT pair (c3 geometry, 16 views) under ncu."""
 import sys, torch
 sys.path.insert(0, ".")
 import paper_2110_09841_b200 as cb

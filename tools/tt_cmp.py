@@ -1,3 +1,5 @@
+"""Compare two TT output dumps (tools/tt_dump.py) from two library builds:
+rel-L2 and max|d|/max|ref| per scene and amplitude."""
 import numpy as np
 a = np.load("gpurun_out/tt_old.npz"); b = np.load("gpurun_out/tt_new.npz")
 for k in a.files:

@@ -1,3 +1,5 @@
+"""Dump TT P/BP outputs on three scenes (small, C-arm, large cone) for
+tools/tt_cmp.py; CVPB_LIB selects the library build."""
 import sys, numpy as np, torch
 sys.path.insert(0, ".")
 import paper_2110_09841_b200 as cb

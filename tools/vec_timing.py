@@ -1,3 +1,5 @@
+"""Timing of the CGLS vector kernels (dot, axpy, xpby, all_finite) on a
+c3-sized stack."""
 import sys, time, torch
 sys.path.insert(0, ".")
 import paper_2110_09841_b200 as cb
