@@ -33,7 +33,13 @@ namespace cvpb {
 
 namespace {
 
-constexpr int BI = 16, BJ = 8, BK = 64;
+#ifndef TT_BI
+#define TT_BI 16
+#endif
+#ifndef TT_BJ
+#define TT_BJ 8
+#endif
+constexpr int BI = TT_BI, BJ = TT_BJ, BK = 64;
 constexpr int NCOL = BI * BJ;
 constexpr int NT = 256;
 constexpr int NWARP = NT / 32;
