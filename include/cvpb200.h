@@ -146,10 +146,10 @@ int cvpb_fill_uniform01(double* out, size_t n, uint64_t seed);
  * third of the free device memory, further capped by the environment variable
  * CVPB_CUT_TABLE_MAX_BYTES; larger jobs run in view chunks). The table stays
  * allocated until the context is destroyed.
- * The first launch per option set with >= 8 views also times the two brick
+ * The first launch per option set with >= 8 views also times the three brick
  * shapes of the kernels on up to 24 of its views (into its own output) and
- * synchronizes the stream once to read the timings; CVPB_CVP_SHAPE=0|1 skips
- * that (e.g. before capturing a CUDA graph). */
+ * synchronizes the stream once to read the timings; CVPB_CVP_SHAPE=0|1|2
+ * skips that (e.g. before capturing a CUDA graph). */
 /* project_cvp_into (cvp.cpp:615-626): overwrites views [view_begin,
  * view_begin+view_count) of d_proj (which points at view 0's image of that
  * range, i.e. the caller's slice). */

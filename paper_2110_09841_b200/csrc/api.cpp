@@ -206,9 +206,10 @@ struct cvpb_context {
     bool base_reaches_source = false;  // (cvp.cpp:82-84), resolved for the whole box
     int n_slots = 0;
     int cvp_tile_need = 0;    // floats, largest brick footprint over the scene
-    int cvp_tile_need_b = 0;  // the same for brick shape B
+    int cvp_tile_need_b = 0;  // the same for brick shapes B and C
+    int cvp_tile_need_c = 0;
     // brick shape per (direction, precision, elevation, radius): 0 = default,
-    // 1 = shape B; chosen by timing both on the scene's first launch
+    // 1 = shape B, 2 = shape C; chosen by timing them on the scene's first launch
     std::map<int, int> cvp_shape;
     double r_min = 0.0;       // smallest source-to-volume-box distance over the views
     double voxel_rows = 0.0;  // mean voxel height in detector rows at the volume centre
@@ -326,6 +327,15 @@ int reserve_cut_table(cvpb_context* ctx, int view_count, void*& mem, size_t& byt
 int prepare_cut_table(cvpb_context* ctx, const cvpb_cvp_options* opts, int view_begin,
                       int view_count, cudaStream_t st);
 
+int cvp_tile_need_of(const cvpb_context* ctx, int shape) {
+    return shape == 1 ? ctx->cvp_tile_need_b : shape == 2 ? ctx->cvp_tile_need_c : ctx->cvp_tile_need;
+}
+
+cudaError_t launch_cvp_shape(const cvpb::CvpLaunch& L, int shape, cudaStream_t st) {
+    return shape == 1 ? cvpb::launch_cvp_b(L, st) : shape == 2 ? cvpb::launch_cvp_c(L, st)
+                                                               : cvpb::launch_cvp(L, st);
+}
+
 int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_policy* exec,
             bool forward, const float* vol_in, float* vol_out, const float* proj_in,
             float* proj_out, int view_begin, int view_count, int accumulate, cudaStream_t st,
@@ -389,7 +399,7 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     const char* forced = std::getenv("CVPB_CVP_SHAPE");
     bool tune = false;
     if (forced) {
-        shape = std::atoi(forced) == 1 ? 1 : 0;
+        shape = std::min(std::max(std::atoi(forced), 0), 2);
     } else if (it == ctx->cvp_shape.end() && view_count >= 8 && (forward || !accumulate) &&
                !vol_in64 && !vol_out64) {
         // the timing launches need the whole range's cut table resident
@@ -405,25 +415,28 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
         cvpb::CvpLaunch T = L;
         T.view_count = std::min(view_count, 24);
         T.accumulate = 0;
-        float ms[2] = {0.f, 0.f};
+        float ms[3] = {0.f, 0.f, 0.f};
         if (!ctx->ev_tune[0])
             for (cudaEvent_t& e : ctx->ev_tune) CVPB_CUDA(cudaEventCreate(&e));
-        for (int pass = 0; pass < 2; ++pass)  // pass 0 warms both up
-            for (int b = 0; b < 2; ++b) {
-                T.tile_need = b ? ctx->cvp_tile_need_b : ctx->cvp_tile_need;
+        for (int pass = 0; pass < 2; ++pass)  // pass 0 warms them up
+            for (int b = 0; b < 3; ++b) {
+                T.tile_need = cvp_tile_need_of(ctx, b);
                 CVPB_CUDA(cudaEventRecord(ctx->ev_tune[0], st));
-                CVPB_CUDA(b ? cvpb::launch_cvp_b(T, st) : cvpb::launch_cvp(T, st));
+                CVPB_CUDA(launch_cvp_shape(T, b, st));
                 CVPB_CUDA(cudaEventRecord(ctx->ev_tune[1], st));
                 CVPB_CUDA(cudaEventSynchronize(ctx->ev_tune[1]));
                 if (pass) CVPB_CUDA(cudaEventElapsedTime(&ms[b], ctx->ev_tune[0], ctx->ev_tune[1]));
             }
-        shape = ms[1] < 0.97f * ms[0] ? 1 : 0;  // shape B only for a clear win
+        // another shape only for a clear (> 3%) win over the default
+        shape = 0;
+        for (int b = 1; b < 3; ++b)
+            if (ms[b] < 0.97f * ms[0] && ms[b] < ms[shape]) shape = b;
         ctx->cvp_shape[shape_key] = shape;
     }
-    if (shape) L.tile_need = ctx->cvp_tile_need_b;
+    L.tile_need = cvp_tile_need_of(ctx, shape);
     const bool keep = L.cut_table_valid != 0;
     key.valid = 0;
-    CVPB_CUDA(shape ? cvpb::launch_cvp_b(L, st) : cvpb::launch_cvp(L, st));
+    CVPB_CUDA(launch_cvp_shape(L, shape, st));
     CVPB_CUDA(cudaEventRecord(ctx->ev_table, st));
     ctx->ev_table_recorded = true;
     if (keep) {
@@ -726,6 +739,10 @@ int cvpb_set_geometry(cvpb_context* ctx, const cvpb_volume_geometry* vol,
     CVPB_CUDA(cudaStreamSynchronize(ctx->stream));
     CVPB_CUDA(cvpb::launch_cvp_tile_need_b(sc, ctx->d_views.p, n_views, ctx->d_flag.p, ctx->stream));
     CVPB_CUDA(cudaMemcpyAsync(&ctx->cvp_tile_need_b, ctx->d_flag.p, sizeof(int), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    CVPB_CUDA(cudaStreamSynchronize(ctx->stream));
+    CVPB_CUDA(cvpb::launch_cvp_tile_need_c(sc, ctx->d_views.p, n_views, ctx->d_flag.p, ctx->stream));
+    CVPB_CUDA(cudaMemcpyAsync(&ctx->cvp_tile_need_c, ctx->d_flag.p, sizeof(int), cudaMemcpyDeviceToHost,
                               ctx->stream));
     CVPB_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->cvp_shape.clear();

@@ -36,12 +36,15 @@
 #include "cvp_device.cuh"
 #include "kernels.hpp"
 
-// The file is compiled twice (Makefile): the default brick shape, and shape
-// B (CVP_CFG_B: 8x8x64 at four CTAs per SM, faster on some scenes); the
-// brick-dependent entry points of the second copy carry a _b suffix and
-// the shape-independent ones exist once.
-#ifdef CVP_CFG_B
+// The file is compiled three times (Makefile): the default brick shape
+// (8x16x64, 256 threads, three CTAs per SM), shape B (CVP_CFG_B: 8x8x64 at
+// four CTAs per SM) and shape C (CVP_CFG_C: 8x24x64, 384 threads, two CTAs
+// per SM); the brick-dependent entry points of the extra copies carry a _b /
+// _c suffix and the shape-independent ones exist once.
+#if defined(CVP_CFG_B)
 #define CVP_PUB(name) name##_b
+#elif defined(CVP_CFG_C)
+#define CVP_PUB(name) name##_c
 #else
 #define CVP_PUB(name) name
 #endif
@@ -942,7 +945,7 @@ cudaError_t CVP_PUB(launch_cvp)(const CvpLaunch& L, cudaStream_t stream) {
     return cudaSuccess;
 }
 
-#ifndef CVP_CFG_B
+#if !defined(CVP_CFG_B) && !defined(CVP_CFG_C)
 cudaError_t launch_cut_table(const CvpLaunch& L, cudaStream_t stream) {
     const int ncols = L.sc.n1 * L.sc.n2;
     if (L.view_count <= 0) return cudaSuccess;
@@ -972,6 +975,6 @@ cudaError_t launch_cut_records(const Scene& sc, const ViewConst* views, int view
                                                        clamp, cap, rows, cols, vol, inv, n_out, err);
     return cudaGetLastError();
 }
-#endif  // !CVP_CFG_B
+#endif  // shape-independent entry points
 
 }  // namespace cvpb

@@ -43,6 +43,10 @@ cudaError_t launch_cvp(const CvpLaunch& L, cudaStream_t stream);
 cudaError_t launch_cvp_tile_need_b(const Scene& sc, const ViewConst* views, int n_views, int* d_need,
                                    cudaStream_t stream);
 cudaError_t launch_cvp_b(const CvpLaunch& L, cudaStream_t stream);
+// and brick shape C (CVP_CFG_C)
+cudaError_t launch_cvp_tile_need_c(const Scene& sc, const ViewConst* views, int n_views, int* d_need,
+                                   cudaStream_t stream);
+cudaError_t launch_cvp_c(const CvpLaunch& L, cudaStream_t stream);
 // Only the cut table of views [L.view_begin, L.view_begin + L.view_count)
 // (must fit L.cut_table_bytes); later launches over subsets reuse it.
 cudaError_t launch_cut_table(const CvpLaunch& L, cudaStream_t stream);

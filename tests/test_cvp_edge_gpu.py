@@ -120,11 +120,12 @@ def test_view_subrange_equals_slice(checker):
     assert empty.shape[0] == 0
 
 
-@pytest.mark.parametrize("shape", ["0", "1"])
-def test_both_brick_shapes_match_reference(checker, monkeypatch, shape):
-    """The library carries two brick shapes (8x16x64 at three CTAs per SM and
-    8x8x64 at four) and times both on a scene's first launches; each must
-    match the reference on its own (CVPB_CVP_SHAPE forces one)."""
+@pytest.mark.parametrize("shape", ["0", "1", "2"])
+def test_every_brick_shape_matches_reference(checker, monkeypatch, shape):
+    """The library carries three brick shapes (8x16x64 at three CTAs per SM,
+    8x8x64 at four, 8x24x64 with 384 threads at two) and times them on a
+    scene's first launches; each must match the reference on its own
+    (CVPB_CVP_SHAPE forces one)."""
     import paper_2110_09841_b200 as cb
     monkeypatch.setenv("CVPB_CVP_SHAPE", shape)
     det = cb.DetectorGeometry.make(40, 52, 1.0, 1.0)

@@ -27,7 +27,7 @@ def test_random_geometry_exact_parity(checker, monkeypatch, seed):
     arc = float(rng.choice([360.0, 200.0, 90.0]))
     opts4 = (int(rng.integers(0, 2)), int(rng.integers(0, 2)), 0, int(rng.integers(0, 2)))
     ex = cb.ExecPolicy(deterministic=bool(rng.integers(0, 2)))
-    monkeypatch.setenv("CVPB_CVP_SHAPE", str(int(rng.integers(0, 2))))
+    monkeypatch.setenv("CVPB_CVP_SHAPE", str(int(rng.integers(0, 3))))
     det = cb.DetectorGeometry.make(rows, cols, pw, ph)
     geom = cb.VolumeGeometry.make(counts, vox)
     views = cb.make_circular_trajectory(sid, sdd, nv, arc, det)

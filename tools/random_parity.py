@@ -33,7 +33,7 @@ for t in range(n_cases):
     arc = float(rng.choice([360.0, 200.0, 90.0]))
     opts4 = (int(rng.integers(0, 2)), int(rng.integers(0, 2)), 0, int(rng.integers(0, 2)))
     det_mode = bool(rng.integers(0, 2))
-    shape = str(int(rng.integers(0, 2)))
+    shape = str(int(rng.integers(0, 3)))
     import os
     os.environ["CVPB_CVP_SHAPE"] = shape
     det = cb.DetectorGeometry.make(rows, cols, pw, ph)
