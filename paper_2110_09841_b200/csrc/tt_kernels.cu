@@ -41,7 +41,10 @@ namespace {
 #endif
 constexpr int BI = TT_BI, BJ = TT_BJ, BK = 64;
 constexpr int NCOL = BI * BJ;
-constexpr int NT = 256;
+#ifndef TT_NT
+#define TT_NT 256
+#endif
+constexpr int NT = TT_NT;
 constexpr int NWARP = NT / 32;
 constexpr int NH = BK / 32;   // voxels per lane along x3
 #ifndef TT_MINB
