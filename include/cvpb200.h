@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define CVPB_ABI_VERSION 1
+#define CVPB_ABI_VERSION 2
 
 typedef enum cvpb_status {
     CVPB_OK = 0,
@@ -171,6 +171,18 @@ int cvpb_backproject_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
                               const cvpb_exec_policy* exec, const double* proj, double* volume,
                               double* view_seconds);
 
+/* Multi-GPU building blocks of the host path (one rank per GPU, views
+ * sharded: each rank's context holds its own view subset). The backward of
+ * the host stack with the float32 partial volume left in d_volume (no D2H):
+ * the caller sums partials across ranks (NCCL reduce-scatter over z-slabs)
+ * and brings its slab back with cvpb_vec_to_host64. Asynchronous on `stream`. */
+int cvpb_backproject_cvp_host_partial(cvpb_context* ctx, const cvpb_cvp_options* opts,
+                                      const cvpb_exec_policy* exec, const double* proj,
+                                      float* d_volume, void* stream);
+/* float32 device vector -> float64 host buffer (pinned: written in place;
+ * pageable: staged through the context). Synchronous. */
+int cvpb_vec_to_host64(cvpb_context* ctx, const float* d_in, double* host, size_t n, void* stream);
+
 /* collect_cut_records (cvp.cpp:652-689) evaluated by the DEVICE kernel's own
  * cut/row code for voxel (i,j,k) under view `view`; clamp = 0 reproduces the
  * reference (no detector clamping). Writes at most cap records, total in *n_out. */
@@ -214,8 +226,8 @@ int cvpb_backproject_tt_host(cvpb_context* ctx, const cvpb_tt_options* opts, con
                              double* volume);
 /* cgls (solver.cpp:55-106) device-resident, host data in / host iterate out. */
 int cvpb_cgls_host(cvpb_context* ctx, int projector, const cvpb_cvp_options* cvp_opts,
-                   int k_per_edge, const double* b, double* x, int iterations,
-                   double* residual_norms);
+                   const cvpb_tt_options* tt_opts, const cvpb_exec_policy* exec, int k_per_edge,
+                   const double* b, double* x, int iterations, double* residual_norms);
 
 /* ---- device vector ops for CGLS (solver.cpp:15-106) ---------------------- */
 /* Compensated float64 dot of two float32 device vectors (dot_kahan,
@@ -241,11 +253,16 @@ int cvpb_vec_sart_update(cvpb_context* ctx, float* x, const float* corr, const f
                          double lambda, int nonneg, size_t n, void* stream);
 
 /* Device-resident CGLS (cgls, solver.cpp:55-106) over the context's scene.
- * projector: 0 = CVP (cvp_opts), 1 = Siddon-K (k_per_edge), 2 = TT.
+ * projector: 0 = CVP (cvp_opts), 1 = Siddon-K (k_per_edge), 2 = TT (tt_opts);
+ * every operator call receives `exec` (NULL = ExecPolicy{}: Siddon K >= 128
+ * is refused unless exec->allow_expensive, like the reference).
+ * gamma / alpha / beta stay on the device (fused vector kernels); the host
+ * reads a status word once per iteration for the reference's early exits.
  * d_b is the data (float32 stack, not modified), d_x receives the iterate;
  * residual_norms[iterations+1] receives ||b - A x_k|| (entry 0 = ||b||).
  * Scratch vectors are owned by the context. */
-int cvpb_cgls(cvpb_context* ctx, int projector, const cvpb_cvp_options* cvp_opts, int k_per_edge,
+int cvpb_cgls(cvpb_context* ctx, int projector, const cvpb_cvp_options* cvp_opts,
+              const cvpb_tt_options* tt_opts, const cvpb_exec_policy* exec, int k_per_edge,
               const float* d_b, float* d_x, int iterations, double* residual_norms, void* stream);
 
 #ifdef __cplusplus

@@ -95,16 +95,19 @@ SIGNATURES = {
     "cvpb_backproject_siddon_host": (C.c_int, [_vp, C.c_int, _P(cvpb_exec_policy), _vp, _vp]),
     "cvpb_project_tt_host": (C.c_int, [_vp, _P(cvpb_tt_options), _vp, _vp]),
     "cvpb_backproject_tt_host": (C.c_int, [_vp, _P(cvpb_tt_options), _vp, _vp]),
-    "cvpb_cgls_host": (C.c_int, [_vp, C.c_int, _P(cvpb_cvp_options), C.c_int, _vp, _vp, C.c_int,
-                                 _dp]),
+    "cvpb_cgls_host": (C.c_int, [_vp, C.c_int, _P(cvpb_cvp_options), _P(cvpb_tt_options),
+                                 _P(cvpb_exec_policy), C.c_int, _vp, _vp, C.c_int, _dp]),
+    "cvpb_backproject_cvp_host_partial": (C.c_int, [_vp, _P(cvpb_cvp_options),
+                                                    _P(cvpb_exec_policy), _vp, _vp, _vp]),
+    "cvpb_vec_to_host64": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp]),
     "cvpb_vec_dot": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _dp, _vp]),
     "cvpb_vec_axpy": (C.c_int, [_vp, C.c_double, _vp, _vp, C.c_size_t, _vp]),
     "cvpb_vec_xpby": (C.c_int, [_vp, _vp, C.c_double, _vp, C.c_size_t, _vp]),
     "cvpb_vec_all_finite": (C.c_int, [_vp, _vp, C.c_size_t, _ip, _vp]),
     "cvpb_vec_sart_residual": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_size_t, _vp]),
     "cvpb_vec_sart_update": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, C.c_int, C.c_size_t, _vp]),
-    "cvpb_cgls": (C.c_int, [_vp, C.c_int, _P(cvpb_cvp_options), C.c_int, _vp, _vp, C.c_int, _dp,
-                            _vp]),
+    "cvpb_cgls": (C.c_int, [_vp, C.c_int, _P(cvpb_cvp_options), _P(cvpb_tt_options),
+                            _P(cvpb_exec_policy), C.c_int, _vp, _vp, C.c_int, _dp, _vp]),
 }
 
 # status code -> exception type the reference throws for the same condition

@@ -229,6 +229,8 @@ struct cvpb_context {
     bool ev_table_recorded = false;
     DevBuf<float> h_vol, h_proj;  // device buffers of the host path
     DevBuf<float> cg_r, cg_q, cg_s, cg_p;
+    DevBuf<double> cg_partials, cg_hist;
+    DevBuf<cvpb::CgState> cg_state;
     DevBuf<int> d_rec_i;
     DevBuf<double> d_rec_d;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -315,6 +317,9 @@ int reserve_cut_table(cvpb_context* ctx, int view_count, void*& mem, size_t& byt
             cap = std::min(cap, size_t(std::strtoull(env, nullptr, 10)));
         if (want > cap) want = std::max(per_view, cap / per_view * per_view);
         if (ctx->d_cut_table.n < want) {
+            // the table's contents go with the old buffer: a later launch
+            // must not trust a key that described it
+            ctx->cut_key.valid = 0;
             ctx->d_cut_table.release();
             CVPB_CUDA(ctx->d_cut_table.reserve(want));
         }
@@ -632,6 +637,9 @@ void cvpb_context_destroy(cvpb_context* ctx) {
     ctx->d_cut_table.release();
     ctx->d_rec_i.release();
     ctx->d_rec_d.release();
+    ctx->cg_partials.release();
+    ctx->cg_hist.release();
+    ctx->cg_state.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     for (cudaEvent_t e : ctx->ev_chunk)
@@ -925,6 +933,8 @@ int cvpb_project_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
     cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
     const size_t nv = ctx->nvox(), npx = ctx->npx_view();
     const int nviews = int(ctx->views.size());
+    // this call reports its own device errors only
+    CVPB_CUDA(cudaMemsetAsync(ctx->d_err.p, 0, sizeof(int), st));
     CVPB_CUDA(cudaEventRecord(ctx->ev0, st));
     // pinned input: the first chunk's bricks read it in place and leave a
     // float32 device copy for the later chunks (pageable input: one bulk
@@ -970,6 +980,7 @@ int cvpb_backproject_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
     cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
     const size_t nv = ctx->nvox(), npx = ctx->npx_view();
     const int nviews = int(ctx->views.size());
+    CVPB_CUDA(cudaMemsetAsync(ctx->d_err.p, 0, sizeof(int), st));
     CVPB_CUDA(cudaEventRecord(ctx->ev0, st));
     CVPB_CUDA(cudaStreamWaitEvent(cs, ctx->ev0, 0));
     // view chunks: chunk c + 1 of the stack comes in (float64 -> float32) on
@@ -1007,6 +1018,59 @@ int cvpb_backproject_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
     return CVPB_OK;
 }
 
+// The host path's backward with the result left in device memory: float64
+// host stack in (view chunks H2D + converted on the copy stream, overlapped
+// with the bricks of the previous chunk), float32 partial volume out on the
+// caller's stream — what a view-sharded rank hands to its cross-device
+// reduce-scatter (bench.py N > 1, parallel.py).
+int cvpb_backproject_cvp_host_partial(cvpb_context* ctx, const cvpb_cvp_options* opts,
+                                      const cvpb_exec_policy* exec, const double* proj,
+                                      float* d_volume, void* stream) {
+    CVPB_TRY(check_ctx(ctx));
+    if (!proj || !d_volume) return fail(CVPB_INVALID_ARGUMENT, "null buffer");
+    CVPB_TRY(ensure_host_buffers(ctx));
+    cudaStream_t st = static_cast<cudaStream_t>(stream), cs = ctx->copy_stream;
+    const size_t npx = ctx->npx_view();
+    const int nviews = int(ctx->views.size());
+    CVPB_CUDA(cudaEventRecord(ctx->ev0, st));
+    CVPB_CUDA(cudaStreamWaitEvent(cs, ctx->ev0, 0));
+    const int n = host_chunks(nviews);
+    for (int c = 0; c < n; ++c) {
+        const int v0 = chunk_begin(nviews, n, c), v1 = chunk_begin(nviews, n, c + 1);
+        const size_t off = npx * size_t(v0), cnt = npx * size_t(v1 - v0);
+        CVPB_CUDA(cudaMemcpyAsync(ctx->d_stage.p + off, proj + off, sizeof(double) * cnt,
+                                  cudaMemcpyHostToDevice, cs));
+        CVPB_CUDA(cvpb::launch_f64_to_f32(ctx->d_stage.p + off, ctx->h_proj.p + off, cnt, cs));
+        CVPB_CUDA(cudaEventRecord(ctx->ev_chunk[c], cs));
+    }
+    if (n > 1) CVPB_TRY(prepare_cut_table(ctx, opts, 0, nviews, st));
+    for (int c = 0; c < n; ++c) {
+        const int v0 = chunk_begin(nviews, n, c), v1 = chunk_begin(nviews, n, c + 1);
+        CVPB_CUDA(cudaStreamWaitEvent(st, ctx->ev_chunk[c], 0));
+        CVPB_TRY(run_cvp(ctx, opts, exec, false, nullptr, d_volume, ctx->h_proj.p + npx * size_t(v0),
+                         nullptr, v0, v1 - v0, c > 0 ? 1 : 0, st));
+    }
+    if (nviews == 0) CVPB_CUDA(cudaMemsetAsync(d_volume, 0, sizeof(float) * ctx->nvox(), st));
+    return CVPB_OK;
+}
+
+// float32 device vector -> float64 host buffer (pinned: written in place by
+// the conversion kernel; pageable: staged), synchronous.
+int cvpb_vec_to_host64(cvpb_context* ctx, const float* d_in, double* host, size_t n, void* stream) {
+    CVPB_TRY(check_ctx(ctx, false));
+    if ((!d_in || !host) && n) return fail(CVPB_INVALID_ARGUMENT, "null buffer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (double* mapped = mapped_host(host)) {
+        CVPB_CUDA(cvpb::launch_f32_to_f64(d_in, mapped, n, st));
+    } else {
+        CVPB_CUDA(ctx->d_stage.reserve(std::max(ctx->d_stage.n, n)));
+        CVPB_CUDA(cvpb::launch_f32_to_f64(d_in, ctx->d_stage.p, n, st));
+        CVPB_CUDA(cudaMemcpyAsync(host, ctx->d_stage.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    }
+    CVPB_CUDA(cudaStreamSynchronize(st));
+    return CVPB_OK;
+}
+
 int cvpb_collect_cut_records(cvpb_context* ctx, const cvpb_cvp_options* opts, int view, int i,
                              int j, int k, int clamp, int cap, int* rows, int* cols,
                              double* volume, double* inv_r2, int* n_out) {
@@ -1019,6 +1083,7 @@ int cvpb_collect_cut_records(cvpb_context* ctx, const cvpb_cvp_options* opts, in
     CVPB_TRY(check_scene_views(ctx));
     if (cap < 0) cap = 0;
     cudaStream_t st = ctx->stream;
+    CVPB_CUDA(cudaMemsetAsync(ctx->d_err.p, 0, sizeof(int), st));
     CVPB_CUDA(ctx->d_rec_i.reserve(2 * size_t(cap) + 1));
     CVPB_CUDA(ctx->d_rec_d.reserve(2 * size_t(cap) + 1));
     int* d_rows = ctx->d_rec_i.p;
@@ -1238,11 +1303,11 @@ int cvpb_backproject_tt_host(cvpb_context* ctx, const cvpb_tt_options* opts, con
 }
 
 int cvpb_cgls_host(cvpb_context* ctx, int projector, const cvpb_cvp_options* cvp_opts,
-                   int k_per_edge, const double* b, double* x, int iterations,
-                   double* residual_norms) {
+                   const cvpb_tt_options* tt_opts, const cvpb_exec_policy* exec, int k_per_edge,
+                   const double* b, double* x, int iterations, double* residual_norms) {
     return host_roundtrip(ctx, false, b, x, [&](float* din, float* dout, cudaStream_t st) {
-        return cvpb_cgls(ctx, projector, cvp_opts, k_per_edge, din, dout, iterations,
-                         residual_norms, st);
+        return cvpb_cgls(ctx, projector, cvp_opts, tt_opts, exec, k_per_edge, din, dout,
+                         iterations, residual_norms, st);
     });
 }
 
@@ -1313,8 +1378,14 @@ int cvpb_vec_sart_update(cvpb_context* ctx, float* x, const float* corr, const f
 }
 
 // ---- device-resident CGLS (solver.cpp:55-106) ------------------------------------
+// Per iteration: A p -> q, q.q partials, alpha (device scalar kernel), one
+// fused pass x += alpha p / r -= alpha q / r.r partials / finite check,
+// A^T r -> s, s.s partials, beta + history entry (device), p = s + beta p.
+// gamma, alpha and beta never leave the device; the host reads the 4-word
+// status once per iteration (the reference's early exits need it).
 
-int cvpb_cgls(cvpb_context* ctx, int projector, const cvpb_cvp_options* cvp_opts, int k_per_edge,
+int cvpb_cgls(cvpb_context* ctx, int projector, const cvpb_cvp_options* cvp_opts,
+              const cvpb_tt_options* tt_opts, const cvpb_exec_policy* exec, int k_per_edge,
               const float* d_b, float* d_x, int iterations, double* residual_norms, void* stream) {
     CVPB_TRY(check_ctx(ctx));
     if (iterations < 1) return fail(CVPB_INVALID_ARGUMENT, "cgls needs at least one iteration");
@@ -1322,66 +1393,69 @@ int cvpb_cgls(cvpb_context* ctx, int projector, const cvpb_cvp_options* cvp_opts
     if (projector < 0 || projector > 2) return fail(CVPB_INVALID_ARGUMENT, "unknown projector");
     cvpb_cvp_options defaults{CVPB_SCALING_EXACT, 1, CVPB_PRECISION_EXACT, CVPB_R_CUT_CENTROID};
     const cvpb_cvp_options* opts = cvp_opts ? cvp_opts : &defaults;
-    cvpb_exec_policy ex{0, 0, 1};
+    CVPB_TRY(check_cvp_options(opts));
+    const cvpb_exec_policy ex = exec ? *exec : cvpb_exec_policy{0, 0, 0};
+    if (projector == 1) CVPB_TRY(check_siddon_k(k_per_edge, &ex));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t n = ctx->nvox(), m = ctx->npx_view() * ctx->views.size();
     const int V = int(ctx->views.size());
+    const int np = cvpb::dot_partials_count();
     CVPB_CUDA(ctx->cg_r.reserve(m));
     CVPB_CUDA(ctx->cg_q.reserve(m));
     CVPB_CUDA(ctx->cg_s.reserve(n));
     CVPB_CUDA(ctx->cg_p.reserve(n));
+    CVPB_CUDA(ctx->cg_partials.reserve(2 * size_t(np)));
+    CVPB_CUDA(ctx->cg_hist.reserve(size_t(iterations) + 1));
+    CVPB_CUDA(ctx->cg_state.reserve(1));
     float *r = ctx->cg_r.p, *q = ctx->cg_q.p, *s = ctx->cg_s.p, *p = ctx->cg_p.p;
+    double *pa = ctx->cg_partials.p, *pb = pa + np, *hist = ctx->cg_hist.p;
+    cvpb::CgState* state = ctx->cg_state.p;
     auto forward = [&](const float* x, float* out) -> int {
         if (projector == 0) return cvpb_project_cvp(ctx, opts, &ex, x, out, 0, V, st);
         if (projector == 1) return cvpb_project_siddon(ctx, k_per_edge, nullptr, &ex, x, out, 0, V, st);
-        return cvpb_project_tt(ctx, nullptr, x, out, 0, V, st);
+        return cvpb_project_tt(ctx, tt_opts, x, out, 0, V, st);
     };
     auto adjoint = [&](const float* b, float* out) -> int {
         if (projector == 0) return cvpb_backproject_cvp(ctx, opts, &ex, b, out, 0, V, 0, st);
         if (projector == 1) return cvpb_backproject_siddon(ctx, k_per_edge, &ex, b, out, 0, V, 0, st);
-        return cvpb_backproject_tt(ctx, nullptr, b, out, 0, V, 0, st);
-    };
-    auto dotv = [&](const float* a, const float* b, size_t len, double* out) {
-        return cvpb_vec_dot(ctx, a, b, len, out, st);
+        return cvpb_backproject_tt(ctx, tt_opts, b, out, 0, V, 0, st);
     };
     CVPB_CUDA(cudaMemcpyAsync(r, d_b, sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
     CVPB_CUDA(cudaMemsetAsync(d_x, 0, sizeof(float) * n, st));
-    double rr;
-    CVPB_TRY(dotv(r, r, m, &rr));
-    residual_norms[0] = std::sqrt(rr);
+    CVPB_CUDA(cudaMemsetAsync(state, 0, sizeof(cvpb::CgState), st));
+    CVPB_CUDA(cvpb::launch_dot(r, r, m, pa, np, st));
+    CVPB_CUDA(cvpb::launch_cg_scalar(0, pa, pb, state, hist, 0, st));
     CVPB_TRY(adjoint(r, s));
     CVPB_CUDA(cudaMemcpyAsync(p, s, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
-    double gamma;
-    CVPB_TRY(dotv(s, s, n, &gamma));
+    CVPB_CUDA(cvpb::launch_dot(s, s, n, pa, np, st));
+    CVPB_CUDA(cvpb::launch_cg_scalar(1, pa, pb, state, hist, 0, st));
+    cvpb::CgState h{};
+    int done = 0;  // iterations whose history entry is final on the device
     for (int it = 1; it <= iterations; ++it) {
-        if (gamma == 0.0) {  // normal equations satisfied: keep the history flat
-            residual_norms[it] = residual_norms[it - 1];
-            continue;
-        }
         CVPB_TRY(forward(p, q));
-        double qq;
-        CVPB_TRY(dotv(q, q, m, &qq));
-        if (qq == 0.0)
-            return fail(CVPB_RUNTIME_ERROR,
-                        "CGLS breakdown (A p = 0) at iteration " + std::to_string(it));
-        const double alpha = gamma / qq;
-        CVPB_CUDA(cvpb::launch_axpy(alpha, p, d_x, n, st));
-        CVPB_CUDA(cvpb::launch_axpy(-alpha, q, r, m, st));
+        CVPB_CUDA(cvpb::launch_dot(q, q, m, pa, np, st));
+        CVPB_CUDA(cvpb::launch_cg_scalar(2, pa, pb, state, hist, it, st));
+        CVPB_CUDA(cvpb::launch_cg_update(state, d_x, p, n, r, q, m, pb, &state->finite, st));
         CVPB_TRY(adjoint(r, s));
-        double gamma_new;
-        CVPB_TRY(dotv(s, s, n, &gamma_new));
-        const double beta = gamma_new / gamma;
-        CVPB_CUDA(cvpb::launch_xpby(s, beta, p, n, st));
-        gamma = gamma_new;
-        int fx = 1, fr = 1;
-        CVPB_TRY(cvpb_vec_all_finite(ctx, d_x, n, &fx, st));
-        CVPB_TRY(cvpb_vec_all_finite(ctx, r, m, &fr, st));
-        if (!fx || !fr)
-            return fail(CVPB_RUNTIME_ERROR,
-                        "CGLS diverged (non-finite iterate) at iteration " + std::to_string(it));
-        CVPB_TRY(dotv(r, r, m, &rr));
-        residual_norms[it] = std::sqrt(rr);
+        CVPB_CUDA(cvpb::launch_dot(s, s, n, pa, np, st));
+        CVPB_CUDA(cvpb::launch_cg_scalar(3, pa, pb, state, hist, it, st));
+        CVPB_CUDA(cvpb::launch_cg_xpby(state, s, p, n, st));
+        CVPB_CUDA(cudaMemcpyAsync(&h, state, sizeof h, cudaMemcpyDeviceToHost, st));
+        CVPB_CUDA(cudaStreamSynchronize(st));
+        done = it;
+        if (h.status != 0) break;
     }
+    CVPB_CUDA(cudaMemcpyAsync(residual_norms, hist, sizeof(double) * (done + 1),
+                              cudaMemcpyDeviceToHost, st));
+    CVPB_CUDA(cudaStreamSynchronize(st));
+    if (h.status == cvpb::kCgBreakdown)
+        return fail(CVPB_RUNTIME_ERROR,
+                    "CGLS breakdown (A p = 0) at iteration " + std::to_string(h.iteration));
+    if (h.status == cvpb::kCgDiverged)
+        return fail(CVPB_RUNTIME_ERROR,
+                    "CGLS diverged (non-finite iterate) at iteration " + std::to_string(h.iteration));
+    for (int it = done + 1; it <= iterations; ++it)  // gamma == 0: the history stays flat
+        residual_norms[it] = residual_norms[it - 1];
     return CVPB_OK;
 }
 

@@ -142,6 +142,7 @@ struct Smem {
     const float* scale;       // backward: this view's phase-2 factors
     int tile_m0, tile_n0, tile_rows, tile_cols, tile_stride, tile_ok;
     float mu_abs_max;         // forward: max |mu| over the brick
+    int nonfinite;            // forward: the brick holds a NaN / Inf attenuation
     float qscale;             // forward: fixed-point scale of this (brick, view)
 };
 
@@ -293,7 +294,10 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
     const size_t plane = size_t(sc.n1) * sc.n2;
     // Stage the brick's voxels: [column][k] with odd stride (bank-conflict free).
     if (tid < NCOL) s.nonzero[tid] = 0;
-    if (tid == 0) s.mu_abs_max = 0.f;
+    if (tid == 0) {
+        s.mu_abs_max = 0.f;
+        s.nonfinite = 0;
+    }
     // forward: the fixed-point tile starts zeroed and every flush re-zeroes
     // the pixels it reads, so views need no zeroing pass of their own
     if (FWD)
@@ -313,6 +317,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 val = __ldg(p.vol_in + off);
             }
             if (val != 0.f) s.nonzero[c] = 1;
+            if (!isfinite(val)) s.nonfinite = 1;
             abs_max = fmaxf(abs_max, fabsf(val));
         }
         s.vox[c * MUS + kk] = val;
@@ -353,6 +358,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
         constexpr bool SPLIT = NCOL < NT && !FWD;
         auto footprint = [&]() {
             int m0, m1, n0, n1;
+            bool fixed_ok = true;
             double dmin = 0.0, dmax = 0.0;
             brick_footprint(vc, sc, i0, i1, j0, j1, k0, k1, m0, m1, n0, n1, &dmin, &dmax);
             if (FWD) {
@@ -369,16 +375,24 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 const double area = vc.b1 * dmax / vc.f * fmax(dmax - dmin, 1e-30 * dmax);
                 const double zwin = vc.b2 * (dmax + 0.5 * diag) / vc.f;
                 const double bound = double(s.mu_abs_max) * area * zwin / (dmin * dmin) * 1.05;
-                s.qscale = (bound > 0.0 && dmin > 0.0) ? float(1073741824.0 / bound) : 0.f;
+                const double q = (bound > 0.0 && dmin > 0.0) ? 1073741824.0 / bound : 0.0;
+                // the fixed-point tile needs a finite brick and a normal
+                // float32 scale; otherwise (NaN / Inf voxels, |mu| so small
+                // that 2^30 / bound overflows) every record of this (brick,
+                // view) takes the float-atomic path below, which propagates
+                // NaN / Inf like the reference's double accumulation
+                fixed_ok = !s.nonfinite && q > 0.0 && q < 3.0e38 && float(q) >= 1.17549435e-38f;
+                s.qscale = fixed_ok ? float(q) : 0.f;
             }
             const int tr = max(m1 - m0 + 1, 0), tc = max(n1 - n0 + 1, 0);
             const int stride = tr | 1;
+            if (FWD && !fixed_ok && s.mu_abs_max == 0.f && !s.nonfinite) fixed_ok = true;  // all-zero brick
             s.tile_m0 = m0;
             s.tile_n0 = n0;
             s.tile_rows = tr;
             s.tile_cols = tc;
             s.tile_stride = stride;
-            s.tile_ok = (tr > 0 && tc > 0 && stride * tc <= p.tile_cap) ? 1 : 0;
+            s.tile_ok = (tr > 0 && tc > 0 && stride * tc <= p.tile_cap && (!FWD || fixed_ok)) ? 1 : 0;
             const size_t vl = size_t(v - p.view_begin);
             s.img = FWD ? p.proj_out + vl * npx : const_cast<float*>(p.proj_in) + vl * npx;
             s.scale = p.scales + size_t(vc.scale_slot) * npx;

@@ -69,19 +69,31 @@ cvpb_exec_policy to_c(const ExecPolicy& e) {
 
 // Device scenes keyed by (volume, detector, views); a small LRU so repeated
 // calls with the same geometry (CGLS, benchmarks) reuse the resident views and
-// pixel-scale images.
+// pixel-scale images. The reference's free functions are reentrant, so each
+// call holds a Lease: a shared_ptr that keeps its entry alive even if the LRU
+// evicts it meanwhile, plus the entry's mutex for the whole call (a context's
+// host-path buffers, cut-table key and scratch are mutable state). Calls on
+// different scenes run concurrently; calls on one scene serialise.
 struct SceneEntry {
     cvpb_volume_geometry vol;
     cvpb_detector_geometry det;
     std::vector<cvpb_view> views;
     cvpb_context* ctx = nullptr;
+    std::mutex mu;
     ~SceneEntry() {
         if (ctx) cvpb_context_destroy(ctx);
     }
 };
 
-std::mutex g_mu;
-std::list<std::unique_ptr<SceneEntry>> g_scenes;
+struct Lease {
+    std::shared_ptr<SceneEntry> entry;
+    std::unique_lock<std::mutex> lock;
+    cvpb_context* get() const { return entry->ctx; }
+    operator cvpb_context*() const { return entry->ctx; }
+};
+
+std::mutex g_mu;  // guards the LRU list only
+std::list<std::shared_ptr<SceneEntry>> g_scenes;
 
 bool same(const SceneEntry& e, const cvpb_volume_geometry& v, const cvpb_detector_geometry& d,
           const std::vector<cvpb_view>& views) {
@@ -90,35 +102,47 @@ bool same(const SceneEntry& e, const cvpb_volume_geometry& v, const cvpb_detecto
            (views.empty() || std::memcmp(e.views.data(), views.data(), sizeof(cvpb_view) * views.size()) == 0);
 }
 
-cvpb_context* scene(const VolumeGeometry& vg, const DetectorGeometry& dg,
-                    std::span<const ViewGeometry> views) {
+Lease scene(const VolumeGeometry& vg, const DetectorGeometry& dg, std::span<const ViewGeometry> views) {
     const cvpb_volume_geometry v = to_c(vg);
     const cvpb_detector_geometry d = to_c(dg);
     std::vector<cvpb_view> cv;
     cv.reserve(views.size());
     for (const auto& x : views) cv.push_back(to_c(x));
-    std::lock_guard<std::mutex> lock(g_mu);
-    for (auto it = g_scenes.begin(); it != g_scenes.end(); ++it)
-        if (same(**it, v, d, cv)) {
-            g_scenes.splice(g_scenes.begin(), g_scenes, it);
-            return g_scenes.front()->ctx;
-        }
-    auto e = std::make_unique<SceneEntry>();
-    e->vol = v;
-    e->det = d;
-    e->views = cv;
-    check(cvpb_context_create(0, &e->ctx));
-    check(cvpb_set_geometry(e->ctx, &v, &d, int(cv.size()), cv.data()));
-    g_scenes.push_front(std::move(e));
-    while (g_scenes.size() > 4) g_scenes.pop_back();
-    return g_scenes.front()->ctx;
+    std::shared_ptr<SceneEntry> e;
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        for (auto it = g_scenes.begin(); it != g_scenes.end(); ++it)
+            if (same(**it, v, d, cv)) {
+                g_scenes.splice(g_scenes.begin(), g_scenes, it);
+                e = g_scenes.front();
+                break;
+            }
+    }
+    if (!e) {
+        // build outside the list lock (uploads views, scale images); a racing
+        // thread may build the same scene, the list then holds both for a while
+        e = std::make_shared<SceneEntry>();
+        e->vol = v;
+        e->det = d;
+        e->views = cv;
+        check(cvpb_context_create(0, &e->ctx));
+        check(cvpb_set_geometry(e->ctx, &v, &d, int(cv.size()), cv.data()));
+        std::lock_guard<std::mutex> lock(g_mu);
+        g_scenes.push_front(e);
+        while (g_scenes.size() > 4) g_scenes.pop_back();  // leases keep evicted entries alive
+    }
+    Lease l{e, std::unique_lock<std::mutex>(e->mu)};
+    return l;
 }
 
-cvpb_context* any_context() {
-    static cvpb_context* ctx = nullptr;
-    std::lock_guard<std::mutex> lock(g_mu);
-    if (!ctx) check(cvpb_context_create(0, &ctx));
-    return ctx;
+// geometry-less context for trace_ray (its scratch is per context: one caller at a time)
+Lease any_context() {
+    static std::shared_ptr<SceneEntry> e = [] {
+        auto p = std::make_shared<SceneEntry>();
+        check(cvpb_context_create(0, &p->ctx));
+        return p;
+    }();
+    return Lease{e, std::unique_lock<std::mutex>(e->mu)};
 }
 
 ViewGeometry from_c(const cvpb_view& c);
@@ -138,6 +162,8 @@ double dot_kahan(std::span<const double> a, std::span<const double> b) {
 
 // ---- geometry -------------------------------------------------------------------
 
+// VolumeGeometry::make / voxel_center and DetectorGeometry::make restate
+// geometry.cpp:23-48 (same checks and messages: the exception contract).
 VolumeGeometry VolumeGeometry::make(std::array<int, 3> counts, Vec3d voxel_size) {
     for (int c : counts)
         if (c <= 0) throw std::invalid_argument("voxel counts must be positive");
@@ -203,6 +229,7 @@ Vec2d ViewGeometry::project_point(const Vec3d& x) const {
     return {chi[0], chi[1]};
 }
 
+// to_local_spherical / elevation_angle / detector_point: geometry.cpp:98-118.
 LocalSpherical ViewGeometry::to_local_spherical(const Vec3d& x) const {
     const Vec3d d = x - source_;
     const double r = norm(d);
@@ -251,6 +278,8 @@ std::vector<ViewGeometry> make_circular_trajectory(double sid, double sdd, int n
     return out;
 }
 
+// Camera-matrix text I/O: geometry.cpp:212-249 (17 significant digits, '#'
+// comments, the reference's error texts).
 void write_camera_matrices(const std::filesystem::path& path, std::span<const ViewGeometry> views) {
     std::ofstream out(path);
     if (!out) throw std::runtime_error("cannot open " + path.string() + " for writing");
@@ -307,6 +336,8 @@ double pixel_scale_exact(const ViewGeometry& view, const DetectorGeometry& det, 
     return out;
 }
 
+// spherical_quad_area: cvp.cpp:580-599 (edge-normal form and domain checks of
+// the public helper; the device scale images use a cancellation-free form).
 double spherical_quad_area(const Vec3d& t0, const Vec3d& t1, const Vec3d& t2, const Vec3d& t3) {
     const Vec3d t[4] = {t0, t1, t2, t3};
     for (const Vec3d& v : t)
@@ -333,7 +364,7 @@ void project_cvp_into(const AttenuationVolume& vol, std::span<const ViewGeometry
     if (out.det != det || out.n_views != int(views.size()))
         throw std::invalid_argument("output stack does not match detector/views");
     if (view_seconds) view_seconds->assign(views.size(), 0.0);
-    cvpb_context* ctx = scene(vol.geom, det, views);
+    Lease ctx = scene(vol.geom, det, views);
     const cvpb_cvp_options o = to_c(opts);
     const cvpb_exec_policy e = to_c(exec);
     check(cvpb_project_cvp_host(ctx, &o, &e, vol.values.data(), out.values.data(),
@@ -356,7 +387,7 @@ void backproject_cvp_into(const ProjectionStack& proj, std::span<const ViewGeome
     if (proj.n_views != int(views.size()))
         throw std::invalid_argument("projection stack does not match views");
     if (view_seconds) view_seconds->assign(views.size(), 0.0);
-    cvpb_context* ctx = scene(vol_geom, proj.det, views);
+    Lease ctx = scene(vol_geom, proj.det, views);
     const cvpb_cvp_options o = to_c(opts);
     const cvpb_exec_policy e = to_c(exec);
     check(cvpb_backproject_cvp_host(ctx, &o, &e, proj.values.data(), out.values.data(),
@@ -378,7 +409,7 @@ std::vector<CutVolumeRecord> collect_cut_records(const VolumeGeometry& vol_geom,
     if (i < 0 || j < 0 || k < 0 || i >= vol_geom.counts[0] || j >= vol_geom.counts[1] ||
         k >= vol_geom.counts[2])
         throw std::out_of_range("voxel index outside lattice");
-    cvpb_context* ctx = scene(vol_geom, det, std::span<const ViewGeometry>(&view, 1));
+    Lease ctx = scene(vol_geom, det, std::span<const ViewGeometry>(&view, 1));
     const cvpb_cvp_options o = to_c(opts);
     int cap = 64, n = 0;
     for (;;) {
@@ -403,7 +434,8 @@ RayIntersectionList trace_ray(const VolumeGeometry& vol, const Vec3d& source, co
     int cap = 4 * (vol.counts[0] + vol.counts[1] + vol.counts[2]) + 8, n = 0;
     std::vector<int> ijk(3 * cap);
     std::vector<double> len(cap);
-    check(cvpb_trace_ray(any_context(), &v, s, t, cap, ijk.data(), len.data(), &n));
+    Lease ctx = any_context();
+    check(cvpb_trace_ray(ctx, &v, s, t, cap, ijk.data(), len.data(), &n));
     RayIntersectionList out(std::min(n, cap));
     for (std::size_t q = 0; q < out.size(); ++q)
         out[q] = {ijk[3 * q], ijk[3 * q + 1], ijk[3 * q + 2], len[q]};
@@ -417,7 +449,7 @@ void project_siddon_k_into(const AttenuationVolume& vol, std::span<const ViewGeo
     if (out.det != det || out.n_views != int(views.size()))
         throw std::invalid_argument("output stack does not match detector/views");
     if (view_seconds) view_seconds->assign(views.size(), 0.0);
-    cvpb_context* ctx = scene(vol.geom, det, views);
+    Lease ctx = scene(vol.geom, det, views);
     const cvpb_exec_policy e = to_c(exec);
     const cvpb_pixel_roi r{roi.row_begin, roi.row_end, roi.col_begin, roi.col_end};
     check(cvpb_project_siddon_host(ctx, k_per_edge, &r, &e, vol.values.data(), out.values.data()));
@@ -438,7 +470,7 @@ void backproject_siddon_k_into(const ProjectionStack& proj, std::span<const View
     if (proj.n_views != int(views.size()))
         throw std::invalid_argument("projection stack does not match views");
     if (view_seconds) view_seconds->assign(views.size(), 0.0);
-    cvpb_context* ctx = scene(vol_geom, proj.det, views);
+    Lease ctx = scene(vol_geom, proj.det, views);
     const cvpb_exec_policy e = to_c(exec);
     check(cvpb_backproject_siddon_host(ctx, k_per_edge, &e, proj.values.data(), out.values.data()));
 }
@@ -544,7 +576,7 @@ namespace b200 {
 ProjectionStack project_tt(const AttenuationVolume& vol, std::span<const ViewGeometry> views,
                            const DetectorGeometry& det, TTAmplitude amp) {
     ProjectionStack out = ProjectionStack::zeros(det, int(views.size()));
-    cvpb_context* ctx = scene(vol.geom, det, views);
+    Lease ctx = scene(vol.geom, det, views);
     const cvpb_tt_options o{int(amp)};
     check(cvpb_project_tt_host(ctx, &o, vol.values.data(), out.values.data()));
     return out;
@@ -555,7 +587,7 @@ AttenuationVolume backproject_tt(const ProjectionStack& proj, std::span<const Vi
     if (proj.n_views != int(views.size()))
         throw std::invalid_argument("projection stack does not match views");
     AttenuationVolume out = AttenuationVolume::zeros(vol_geom);
-    cvpb_context* ctx = scene(vol_geom, proj.det, views);
+    Lease ctx = scene(vol_geom, proj.det, views);
     const cvpb_tt_options o{int(amp)};
     check(cvpb_backproject_tt_host(ctx, &o, proj.values.data(), out.values.data()));
     return out;
@@ -599,13 +631,13 @@ CglsResult cgls_device(const VolumeGeometry& vol, const DetectorGeometry& det,
     if (iterations < 1) throw std::invalid_argument("cgls needs at least one iteration");
     if (b.det != det || b.n_views != int(views.size()))
         throw std::invalid_argument("cgls data does not match the operator range");
-    cvpb_context* ctx = scene(vol, det, views);
+    Lease ctx = scene(vol, det, views);
     const cvpb_cvp_options o = to_c(opts);
     CglsResult res;
     res.x = AttenuationVolume::zeros(vol);
     res.residual_norms.assign(iterations + 1, 0.0);
-    check(cvpb_cgls_host(ctx, 0, &o, 1, b.values.data(), res.x.values.data(), iterations,
-                         res.residual_norms.data()));
+    check(cvpb_cgls_host(ctx, 0, &o, nullptr, nullptr, 1, b.values.data(), res.x.values.data(),
+                         iterations, res.residual_norms.data()));
     return res;
 }
 

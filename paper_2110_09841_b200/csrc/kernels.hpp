@@ -95,6 +95,24 @@ struct TTLaunch {
 cudaError_t launch_tt(const TTLaunch& L, bool forward, cudaStream_t stream);
 
 // vector ops (CGLS)
+// Device-resident CGLS scalars (cvpb_cgls): status 0 = running, else the
+// reference's early exits (solver.cpp:80-105) with the iteration they hit.
+enum { kCgFlat = 1, kCgBreakdown = 2, kCgDiverged = 3 };
+struct CgState {
+    double gamma, alpha, beta;
+    int status, iteration;
+    int finite;
+    int pad;
+};
+// mode 0: hist[0] = sqrt(sum p1); 1: gamma = sum p1; 2: qq = sum p1 -> alpha;
+// 3: gamma_new = sum p1 -> beta, hist[it] = sqrt(sum p2), finite check
+cudaError_t launch_cg_scalar(int mode, const double* p1, const double* p2, CgState* st,
+                             double* hist, int it, cudaStream_t stream);
+cudaError_t launch_cg_update(const CgState* st, float* x, const float* p, size_t n, float* r,
+                             const float* q, size_t m, double* partials, int* finite,
+                             cudaStream_t stream);
+cudaError_t launch_cg_xpby(const CgState* st, const float* s, float* p, size_t n,
+                           cudaStream_t stream);
 cudaError_t launch_dot(const float* a, const float* b, size_t n, double* d_partials,
                        int n_partials, cudaStream_t stream);
 int dot_partials_count();

@@ -77,6 +77,7 @@ struct TTSmem {
     int tile_m0, tile_n0, tile_rows, tile_cols, tile_stride, tile_ok;
     float mu_abs_max;         // forward: max |mu| over the brick
     float qscale;             // forward: fixed-point scale of this (brick, view)
+    int nonfinite;            // forward: the brick holds a NaN / Inf attenuation
 };
 
 __device__ __forceinline__ void red_s32(int* a, int v) {
@@ -225,7 +226,10 @@ __global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
     const int vg1 = min(vg0 + p.views_per_group, p.view_begin + p.view_count);
     if (vg0 >= vg1) return;
     const size_t plane = size_t(sc.n1) * sc.n2;
-    if (tid == 0) s.mu_abs_max = 0.f;
+    if (tid == 0) {
+        s.mu_abs_max = 0.f;
+        s.nonfinite = 0;
+    }
     __syncthreads();
     float abs_max = 0.f;
     for (int idx = tid; idx < NCOL * BK; idx += NT) {
@@ -235,6 +239,7 @@ __global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
         if (FWD && i < i1 && j < j1 && k < k1)
             val = __ldg(p.vol_in + size_t(k) * plane + size_t(j) * sc.n1 + i);
         s.vox[c * MUS + kk] = val;
+        if (!isfinite(val)) s.nonfinite = 1;
         abs_max = fmaxf(abs_max, fabsf(val));
     }
     if (FWD) {
@@ -269,6 +274,7 @@ __global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
                 // footprint rectangle of the brick (corner projections)
                 double cmin = INFINITY, cmax = -INFINITY, rmin = INFINITY, rmax = -INFINITY;
                 double dn = INFINITY, df = -INFINITY, zmax = 0.0;
+                bool fixed_ok = true;
                 for (int q = 0; q < 8; ++q) {
                     const double x = sc.minx + ((q & 1) ? i1 : i0) * sc.a1 - vc.sx;
                     const double y = sc.miny + ((q & 2) ? j1 : j0) * sc.a2 - vc.sy;
@@ -296,7 +302,12 @@ __global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
                     const double amax = diag * sqrt(1.0 + vmax * vmax * vc.b2 * vc.b2 / (vc.f * vc.f));
                     const double wd = (df / dn) * (1.0 + 2.0 * zmax * (df - dn) / (df * sc.a3));
                     const double bound = double(s.mu_abs_max) * amax * double(BI + BJ) * (wd + 2.0) * 1.05;
-                    s.qscale = (bound > 0.0 && dn > 0.0) ? float(1073741824.0 / bound) : 0.f;
+                    const double q = (bound > 0.0 && dn > 0.0) ? 1073741824.0 / bound : 0.0;
+                    // NaN / Inf voxels or a scale outside the normal float32
+                    // range: this (brick, view) scatters with float atomics
+                    fixed_ok = (!s.nonfinite && q > 0.0 && q < 3.0e38 && float(q) >= 1.17549435e-38f) ||
+                               (s.mu_abs_max == 0.f && !s.nonfinite);
+                    s.qscale = fixed_ok && q > 0.0 ? float(q) : 0.f;
                 }
                 const int n0 = max(int(ceil(cmin - 0.5)) - 1, 0), n1 = min(int(floor(cmax + 0.5)) + 1, cols - 1);
                 const int m0 = max(int(ceil(rmin - 0.5)) - 1, 0), m1 = min(int(floor(rmax + 0.5)) + 1, rows - 1);
@@ -306,7 +317,7 @@ __global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
                 s.tile_rows = tr;
                 s.tile_cols = tc;
                 s.tile_stride = tr | 1;
-                s.tile_ok = (tr > 0 && tc > 0 && (tr | 1) * tc <= p.tile_cap) ? 1 : 0;
+                s.tile_ok = (tr > 0 && tc > 0 && (tr | 1) * tc <= p.tile_cap && fixed_ok) ? 1 : 0;
             }
             asm volatile("bar.sync 1, %0;" ::"r"(NT - NCOL) : "memory");
             if (s.tile_ok) {

@@ -97,12 +97,20 @@ class CutVolumeRecord:
     inv_r2: float
 
 
-def _ptr(t):
+def _ptr(t, numel=None, device=None, at_least=False):
+    """Device pointer of a contiguous float32 CUDA tensor; with numel / device
+    the tensor must also hold exactly (at_least: at least) that many elements
+    on that GPU (the kernels index the full scene, so a short or foreign buffer
+    is refused here instead of being read or written out of bounds)."""
     import torch
     if not isinstance(t, torch.Tensor):
         raise InvalidArgument("expected a torch tensor")
     if not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
         raise InvalidArgument("device buffers must be contiguous float32 CUDA tensors")
+    if numel is not None and (t.numel() < numel if at_least else t.numel() != numel):
+        raise InvalidArgument(f"device buffer holds {t.numel()} elements, the scene needs {numel}")
+    if device is not None and (t.device.index if t.device.index is not None else 0) != device:
+        raise InvalidArgument(f"device buffer lives on cuda:{t.device.index}, the scene on cuda:{device}")
     return C.c_void_p(t.data_ptr())
 
 
@@ -165,6 +173,14 @@ class DeviceScene:
             view_count = self.n_views - view_begin
         return int(view_begin), int(view_count)
 
+    def _vol(self, t):
+        return _ptr(t, self.vol_geom.voxel_count(), self.device)
+
+    def _stk(self, t, n_views):
+        # a stack argument points at the first view of the launch's range
+        # (cvpb200.h); a longer buffer is fine, a shorter one is not
+        return _ptr(t, self.det.pixel_count() * max(int(n_views), 0), self.device, at_least=True)
+
     # ---- CVP -------------------------------------------------------------
     def project_cvp(self, vol, out=None, opts: CvpOptions = None, exec: ExecPolicy = None,
                     view_begin=0, view_count=None, stream=None):
@@ -174,7 +190,7 @@ class DeviceScene:
         if out is None:
             out = self.new_stack(vc)
         N.check(N.lib().cvpb_project_cvp(self._h, C.byref(opts._c()), C.byref(exec._c()),
-                                         _ptr(vol), _ptr(out), vb, vc, _stream(stream)))
+                                         self._vol(vol), self._stk(out, vc), vb, vc, _stream(stream)))
         return out
 
     def backproject_cvp(self, proj, out=None, opts: CvpOptions = None, exec: ExecPolicy = None,
@@ -185,8 +201,8 @@ class DeviceScene:
         if out is None:
             out = self.new_volume()
         N.check(N.lib().cvpb_backproject_cvp(self._h, C.byref(opts._c()), C.byref(exec._c()),
-                                             _ptr(proj), _ptr(out), vb, vc, int(bool(accumulate)),
-                                             _stream(stream)))
+                                             self._stk(proj, vc), self._vol(out), vb, vc,
+                                             int(bool(accumulate)), _stream(stream)))
         return out
 
     def project_cvp_host(self, vol64: np.ndarray, out64: np.ndarray = None,
@@ -254,8 +270,8 @@ class DeviceScene:
         r = roi._c() if roi is not None else None
         N.check(N.lib().cvpb_project_siddon(self._h, int(k_per_edge),
                                             C.byref(r) if r is not None else None,
-                                            C.byref(exec._c()), _ptr(vol), _ptr(out), vb, vc,
-                                            _stream(stream)))
+                                            C.byref(exec._c()), self._vol(vol), self._stk(out, vc), vb,
+                                            vc, _stream(stream)))
         return out
 
     def backproject_siddon(self, proj, k_per_edge: int, out=None, exec: ExecPolicy = None,
@@ -265,7 +281,7 @@ class DeviceScene:
         if out is None:
             out = self.new_volume()
         N.check(N.lib().cvpb_backproject_siddon(self._h, int(k_per_edge), C.byref(exec._c()),
-                                                _ptr(proj), _ptr(out), vb, vc,
+                                                self._stk(proj, vc), self._vol(out), vb, vc,
                                                 int(bool(accumulate)), _stream(stream)))
         return out
 
@@ -276,7 +292,8 @@ class DeviceScene:
         vb, vc = self._range(view_begin, view_count)
         if out is None:
             out = self.new_stack(vc)
-        N.check(N.lib().cvpb_project_tt(self._h, C.byref(opts._c()), _ptr(vol), _ptr(out), vb, vc,
+        N.check(N.lib().cvpb_project_tt(self._h, C.byref(opts._c()), self._vol(vol),
+                                        self._stk(out, vc), vb, vc,
                                         _stream(stream)))
         return out
 
@@ -286,7 +303,8 @@ class DeviceScene:
         vb, vc = self._range(view_begin, view_count)
         if out is None:
             out = self.new_volume()
-        N.check(N.lib().cvpb_backproject_tt(self._h, C.byref(opts._c()), _ptr(proj), _ptr(out),
+        N.check(N.lib().cvpb_backproject_tt(self._h, C.byref(opts._c()), self._stk(proj, vc),
+                                            self._vol(out),
                                             vb, vc, int(bool(accumulate)), _stream(stream)))
         return out
 
@@ -314,15 +332,21 @@ class DeviceScene:
         return bool(out.value)
 
     def cgls(self, b, iterations: int, projector: str = "cvp", opts: CvpOptions = None,
-             k_per_edge: int = 1, x=None, stream=None):
-        """Device-resident CGLS (solver.cpp:55-106); returns (x, residual_norms)."""
+             k_per_edge: int = 1, x=None, stream=None, tt_opts: "TTOptions" = None,
+             exec: ExecPolicy = None):
+        """Device-resident CGLS (solver.cpp:55-106); returns (x, residual_norms).
+        Every operator call uses the given options and ExecPolicy (the same
+        operator the pair's own forward/adjoint apply)."""
         pid = {"cvp": 0, "siddon": 1, "tt": 2}[projector]
         opts = opts or CvpOptions()
+        tt_opts = tt_opts or TTOptions()
+        exec = exec or ExecPolicy()
         if x is None:
             x = self.new_volume()
         res = (C.c_double * (iterations + 1))()
-        N.check(N.lib().cvpb_cgls(self._h, pid, C.byref(opts._c()), int(k_per_edge), _ptr(b),
-                                  _ptr(x), int(iterations), res, _stream(stream)))
+        N.check(N.lib().cvpb_cgls(self._h, pid, C.byref(opts._c()), C.byref(tt_opts._c()),
+                                  C.byref(exec._c()), int(k_per_edge), self._stk(b, self.n_views),
+                                  self._vol(x), int(iterations), res, _stream(stream)))
         return x, list(res)
 
 

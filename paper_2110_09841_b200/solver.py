@@ -33,6 +33,8 @@ class LinearOperatorPair:
     projector: str = ""
     cvp_opts: Optional[CvpOptions] = None
     k_per_edge: int = 1
+    tt_opts: Optional[TTOptions] = None
+    exec: Optional[ExecPolicy] = None
 
     def domain_size(self):
         return self.vol_geom.voxel_count()
@@ -48,7 +50,7 @@ def cvp_pair(scene: DeviceScene, opts: CvpOptions = None, exec: ExecPolicy = Non
         forward=lambda x, out: scene.project_cvp(x.values, out.values, opts, exec),
         adjoint=lambda b, out: scene.backproject_cvp(b.values, out.values, opts, exec),
         vol_geom=scene.vol_geom, det=scene.det, n_views=scene.n_views, scene=scene,
-        projector="cvp", cvp_opts=opts)
+        projector="cvp", cvp_opts=opts, exec=exec)
 
 
 def siddon_pair(scene: DeviceScene, k_per_edge: int, exec: ExecPolicy = None) -> LinearOperatorPair:
@@ -57,7 +59,7 @@ def siddon_pair(scene: DeviceScene, k_per_edge: int, exec: ExecPolicy = None) ->
         forward=lambda x, out: scene.project_siddon(x.values, k_per_edge, out.values, None, exec),
         adjoint=lambda b, out: scene.backproject_siddon(b.values, k_per_edge, out.values, exec),
         vol_geom=scene.vol_geom, det=scene.det, n_views=scene.n_views, scene=scene,
-        projector="siddon", k_per_edge=k_per_edge)
+        projector="siddon", k_per_edge=k_per_edge, exec=exec)
 
 
 def tt_pair(scene: DeviceScene, opts: TTOptions = None) -> LinearOperatorPair:
@@ -66,7 +68,7 @@ def tt_pair(scene: DeviceScene, opts: TTOptions = None) -> LinearOperatorPair:
         forward=lambda x, out: scene.project_tt(x.values, out.values, opts),
         adjoint=lambda b, out: scene.backproject_tt(b.values, out.values, opts),
         vol_geom=scene.vol_geom, det=scene.det, n_views=scene.n_views, scene=scene,
-        projector="tt")
+        projector="tt", tt_opts=opts)
 
 
 def fill_uniform01(n: int, seed: int) -> np.ndarray:
@@ -170,7 +172,8 @@ def cgls(pair: LinearOperatorPair, b: ProjectionStack, iterations: int, device: 
         bt = torch.from_numpy(np.asarray(bt, dtype=np.float32))
     bt = bt.reshape(pair.n_views, pair.det.rows, pair.det.cols).to(dev, torch.float32).contiguous()
     if pair.scene is not None and pair.projector in ("cvp", "siddon", "tt"):
-        x, res = pair.scene.cgls(bt, iterations, pair.projector, pair.cvp_opts, pair.k_per_edge)
+        x, res = pair.scene.cgls(bt, iterations, pair.projector, pair.cvp_opts, pair.k_per_edge,
+                                 tt_opts=pair.tt_opts, exec=pair.exec)
         return CglsResult(AttenuationVolume(pair.vol_geom, x), res)
     # generic pair: same recurrence with the device vector kernels
     h = _VecCtx.get(device)

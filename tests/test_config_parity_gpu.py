@@ -1,0 +1,163 @@
+"""GPU parity on the launches the benchmark and BASELINE.json actually run.
+
+Each test runs the FULL configuration on the device — every view of the
+configuration in one launch, with the cut table, brick-shape choice and view
+chunking that launch really uses — and compares an evenly spaced sample of its
+views against the reference (oracle/_ref, the reference compiled from its own
+sources) computed on those views alone:
+
+* forward: views of the full-launch output vs the reference projection of the
+  sampled views;
+* backward: the full-launch backprojection of a stack that is zero outside the
+  sampled views vs the reference backprojection of those views' images (the
+  zero views still run through every brick: one CTA walks all of them).
+
+Tolerance (north star): rel-L2 <= 1e-5 and max|d|/max|ref| <= 1e-4 against the
+reference Double, for exact AND relaxed precision.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import max_rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+L2, MX = 1e-5, 1e-4
+THREADS = os.cpu_count() or 1
+
+
+def _setup(counts, voxel, rows, cols, pw, ph, sid, sdd, nv, arc):
+    import paper_2110_09841_b200 as cb
+    det = cb.DetectorGeometry.make(rows, cols, pw, ph)
+    geom = cb.VolumeGeometry.make(counts, voxel)
+    views = cb.make_circular_trajectory(sid, sdd, nv, arc, det)
+    return cb, geom, det, views
+
+
+def _sample_scene(cb, geom, det, views, idx):
+    from oracle.pyoracle import Scene
+    sub = [views[i] for i in idx]
+    return Scene(tuple(geom.counts), tuple(geom.voxel_size), det.rows, det.cols, det.pixel_width,
+                 det.pixel_height, cb.views_to_array(sub))
+
+
+def _check(got, ref, what):
+    a, b = rel_l2(got, ref), max_rel(got, ref)
+    assert a <= L2 and b <= MX, f"{what}: rel-L2 {a:.3e} max {b:.3e}"
+    return a, b
+
+
+def _full_launch_parity(reference, cfg, idx, precisions=("exact", "relaxed"), seed_x=7, seed_b=8):
+    import torch
+    cb, geom, det, views = _setup(*cfg)
+    V = len(views)
+    scene = cb.DeviceScene(geom, det, views)
+    x32 = cb.fill_uniform01(geom.voxel_count(), seed_x).astype(np.float32)
+    xd = torch.from_numpy(x32).reshape(geom.shape()).cuda()
+    npx = det.pixel_count()
+    b32 = cb.fill_uniform01(npx * len(idx), seed_b).astype(np.float32).reshape(len(idx), det.rows,
+                                                                             det.cols)
+    bd = torch.zeros((V, det.rows, det.cols), dtype=torch.float32, device="cuda")
+    bd[torch.as_tensor(idx, device="cuda")] = torch.from_numpy(b32).cuda()
+    sc = _sample_scene(cb, geom, det, views, idx)
+    p_ref = reference.project_cvp(sc, x32.astype(np.float64), (1, 1, 0, 1), threads=THREADS)
+    bp_ref = reference.backproject_cvp(sc, b32.astype(np.float64).ravel(), (1, 1, 0, 1),
+                                       threads=THREADS)
+    out = {}
+    for prec in precisions:
+        opts = cb.CvpOptions(precision=cb.CvpPrecision.Double if prec == "exact"
+                             else cb.CvpPrecision.Single)
+        p = scene.project_cvp(xd, opts=opts)
+        got = p[torch.as_tensor(idx, device="cuda")].double().cpu().numpy()
+        del p
+        out[prec, "P"] = _check(got, p_ref, f"{prec} P")
+        bp = scene.backproject_cvp(bd, opts=opts).double().cpu().numpy()
+        out[prec, "BP"] = _check(bp.reshape(bp_ref.shape), bp_ref, f"{prec} BP")
+        del bp
+        torch.cuda.empty_cache()
+    scene.close()
+    return out
+
+
+C3 = ((512, 512, 512), (0.09, 0.09, 0.09), 480, 616, 0.154, 0.154, 749.0, 1198.0, 496, 360.0)
+
+
+def test_c3_full_launch_sampled_views(reference):
+    """configs[2], the bench launch: 496 views in one launch, views 0, 62, ..., 434."""
+    _full_launch_parity(reference, C3, list(range(0, 496, 62)))
+
+
+def test_c2_full_launch_sampled_views(reference):
+    """configs[1]: 256^3 @0.18 mm, 616x480 @0.154 mm, 248 views over a 200 deg
+    short scan (SURVEY §8d pinned inputs)."""
+    cfg = ((256, 256, 256), (0.18, 0.18, 0.18), 480, 616, 0.154, 0.154, 749.0, 1198.0, 248, 200.0)
+    _full_launch_parity(reference, cfg, [0, 62, 124, 186, 247])
+
+
+def test_c4_full_launch_sampled_views(reference):
+    """configs[3]: 512^3 @0.5 mm, 1024x1024 @1 mm, SID 300 / SDD 500 (half-cone
+    ~46 deg at the panel edge), 360 views."""
+    cfg = ((512, 512, 512), (0.5, 0.5, 0.5), 1024, 1024, 1.0, 1.0, 300.0, 500.0, 360, 360.0)
+    _full_launch_parity(reference, cfg, [0, 45, 180, 315], precisions=("exact",))
+
+
+def test_c5_full_launch_two_chunk_cut_table(reference, monkeypatch):
+    """configs[4] scene: 1024^3 @0.4 mm, 1024x768 @1 mm, 720 views, with the cut
+    table capped so the launch runs in two view chunks (each chunk rebuilds
+    its table)."""
+    ncols = 1024 * 1024
+    per_view = ncols * 144
+    monkeypatch.setenv("CVPB_CUT_TABLE_MAX_BYTES", str(per_view * 360))
+    cfg = ((1024, 1024, 1024), (0.4, 0.4, 0.4), 768, 1024, 1.0, 1.0, 541.0, 949.0, 720, 360.0)
+    _full_launch_parity(reference, cfg, [100, 500], precisions=("exact",))
+
+
+def test_high_dynamic_range_insert_per_pixel(reference):
+    """A 1e4-contrast insert in a uniform background: the forward's int32
+    fixed-point tile is scaled per (brick, view) by the brick's max |mu|, so
+    low-mu voxels sharing a brick with the insert are quantised relative to
+    it. Per-pixel relative error <= 1e-4 on every pixel >= 1e-3 of the max."""
+    import torch
+    cfg = ((64, 64, 64), (0.72, 0.72, 0.72), 480, 616, 0.154, 0.154, 749.0, 1198.0, 8, 360.0)
+    cb, geom, det, views = _setup(*cfg)
+    x = (0.5 + 0.5 * cb.fill_uniform01(geom.voxel_count(), 11)).reshape(64, 64, 64)
+    x[30:34, 28:36, 20:24] = 1e4          # insert straddling several bricks
+    x[5:9, 50:54, 40:60] = 1e-4 * x[5:9, 50:54, 40:60]  # a very low-mu pocket too
+    x32 = x.astype(np.float32)
+    scene = cb.DeviceScene(geom, det, views)
+    p = scene.project_cvp(torch.from_numpy(x32).cuda()).double().cpu().numpy()
+    sc = _sample_scene(cb, geom, det, views, list(range(len(views))))
+    p_ref = reference.project_cvp(sc, x32.astype(np.float64).ravel(), (1, 1, 0, 1), threads=THREADS)
+    mask = np.abs(p_ref) >= 1e-3 * np.abs(p_ref).max()
+    rel = np.abs(p - p_ref)[mask] / np.abs(p_ref)[mask]
+    assert mask.sum() > 1000
+    assert rel.max() <= 1e-4, (rel.max(), np.percentile(rel, 99.9))
+
+
+def test_nonfinite_and_tiny_volumes_forward():
+    """NaN / Inf voxels propagate like the reference's double accumulation
+    (their bricks leave the fixed-point tile), and a volume scaled by 1e-30
+    projects to 1e-30 times the unscaled projection (no scale overflow)."""
+    import torch
+    cfg = ((32, 32, 32), (1.0, 1.0, 1.0), 48, 48, 1.0, 1.0, 60.0, 100.0, 6, 360.0)
+    cb, geom, det, views = _setup(*cfg)
+    scene = cb.DeviceScene(geom, det, views)
+    x = torch.from_numpy(cb.fill_uniform01(geom.voxel_count(), 5).astype(np.float32)).reshape(
+        geom.shape()).cuda()
+    ref = scene.project_cvp(x)
+    tiny = scene.project_cvp(x * 1e-30)
+    assert torch.isfinite(tiny).all()
+    assert float((tiny.double() * 1e30 - ref.double()).norm() / ref.double().norm()) < 1e-5
+    xn = x.clone()
+    xn[16, 16, 16] = float("nan")
+    pn = scene.project_cvp(xn)
+    assert torch.isnan(pn).any()
+    # pixels whose rays miss the NaN voxel stay equal to the finite projection
+    ok = ~torch.isnan(pn)
+    assert float((pn[ok] - ref[ok]).abs().max() / ref.abs().max()) < 1e-5
+    xi = x.clone()
+    xi[16, 16, 16] = float("inf")
+    pi = scene.project_cvp(xi)
+    assert torch.isinf(pi).any() and not torch.isnan(pi).any()

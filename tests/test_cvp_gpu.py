@@ -1,10 +1,10 @@
 """GPU parity of the CVP pair against the CPU checker (the reference compiled
 from /root/reference when available, else the C restatement).
 
-Tolerances (north star, stated here): exact mode vs reference Double —
-rel-L2 <= 1e-5 and max|d|/max|ref| <= 1e-4 on float32 outputs. Relaxed mode
-vs reference Double — the reference's own Single bound, per-view
-rel-Frobenius <= 1e-3 (test_cvp.cpp:434-458).
+Tolerances (north star, stated here): exact AND relaxed mode vs reference
+Double — rel-L2 <= 1e-5 and max|d|/max|ref| <= 1e-4 on float32 outputs (the
+reference's own Single-vs-Double bound, per-view rel-Frobenius <= 1e-3 of
+test_cvp.cpp:434-458, is far looser).
 """
 import numpy as np
 import pytest
@@ -116,16 +116,23 @@ def test_large_cone_angle_exact(checker):
     assert rel_l2(bp, bp_ref) <= EXACT_L2 and max_rel(bp, bp_ref) <= EXACT_MAX
 
 
-@pytest.mark.parametrize("opts4", [(1, 1, 1, 1), (0, 0, 1, 0)])
-def test_relaxed_tracks_double(checker, opts4):
+@pytest.mark.parametrize("opts4", [(1, 1, 1, 1), (0, 0, 1, 0), (1, 0, 1, 1), (0, 1, 1, 0)])
+def test_relaxed_meets_the_exact_bar(checker, opts4):
+    """Relaxed (Single) device results against the reference DOUBLE at the
+    north-star bar (rel-L2 <= 1e-5, max <= 1e-4) — the device's float32 path is
+    offset-stable, so it does not inherit the reference Single's ~5e-5 gap
+    (that gap is reported, not gated: profiles/parity_*.md)."""
     exact4 = (opts4[0], opts4[1], 0, opts4[3])
-    p, _, bp, _, _ = _run_pair(checker, (64, 64, 64), (0.5, 0.5, 0.5), 128, 128, 1.0, 1.0, 541.0,
-                               949.0, 6, opts4)
-    _, p_ref, _, bp_ref, _ = _run_pair(checker, (64, 64, 64), (0.5, 0.5, 0.5), 128, 128, 1.0, 1.0,
-                                       541.0, 949.0, 6, exact4)
-    for v in range(6):
-        assert rel_l2(p[v], p_ref[v]) < 1e-3
-    assert rel_l2(bp, bp_ref) < 1e-3
+    for case in (((64, 64, 64), (0.5, 0.5, 0.5), 128, 128, 1.0, 1.0, 541.0, 949.0, 6),
+                 ((64, 64, 64), (0.72, 0.72, 0.72), 480, 616, 0.154, 0.154, 749.0, 1198.0, 4)):
+        p, _, bp, _, _ = _run_pair(checker, *case, opts4)
+        _, p_ref, _, bp_ref, _ = _run_pair(checker, *case, exact4)
+        assert rel_l2(p, p_ref) <= EXACT_L2 and max_rel(p, p_ref) <= EXACT_MAX, (
+            case, rel_l2(p, p_ref), max_rel(p, p_ref))
+        assert rel_l2(bp, bp_ref) <= EXACT_L2 and max_rel(bp, bp_ref) <= EXACT_MAX, (
+            case, rel_l2(bp, bp_ref), max_rel(bp, bp_ref))
+        for v in range(p.shape[0]):  # and per view (test_cvp.cpp:434-458 shape)
+            assert rel_l2(p[v], p_ref[v]) <= 1e-4
 
 
 def test_adjoint_identity_device():
