@@ -1,3 +1,3 @@
-// Drop-in forwarder: the reference header cbct/vec.hpp maps onto the GPU-backed API.
+// Drop-in forwarder: the reference header cbct/vec.hpp maps onto cbct_b200/vec.hpp.
 #pragma once
-#include "cbct_b200/cbct.hpp"
+#include "cbct_b200/vec.hpp"

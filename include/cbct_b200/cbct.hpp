@@ -8,9 +8,11 @@
 // the reference's; the numeric work runs on the GPU through libcvpb200's C ABI
 // (include/cvpb200.h). See INTEGRATION.md.
 //
-// Not provided: the reference's test-only introspection helpers column_cuts,
-// row_breakpoints and elevation_corrected_split (cvp.hpp:48-79, exercised only
-// by its unit tests) and the DEN / logging utilities.
+// Also provided (host float64, csrc/dropin/): the polygon kernel
+// (cbct_b200/polygon.hpp), the CVP introspection helpers column_cuts,
+// row_breakpoints and elevation_corrected_split (cvp.hpp:48-79), DEN I/O
+// (cbct_b200/den.hpp) and logging (cbct_b200/log.hpp), so the reference's own
+// callers — its unit tests and acceptance harness — compile unchanged.
 #pragma once
 
 #include <array>
@@ -24,70 +26,10 @@
 #include <stdexcept>
 #include <vector>
 
+#include "cbct_b200/polygon.hpp"
+#include "cbct_b200/vec.hpp"
+
 namespace cbct {
-
-// ---- small vector math (vec.hpp) ------------------------------------------
-template <typename T> struct Vec2 {
-    T x{}, y{};
-    constexpr bool operator==(const Vec2&) const = default;
-    friend constexpr Vec2 operator+(Vec2 a, Vec2 b) { return {a.x + b.x, a.y + b.y}; }
-    friend constexpr Vec2 operator-(Vec2 a, Vec2 b) { return {a.x - b.x, a.y - b.y}; }
-    friend constexpr Vec2 operator-(Vec2 a) { return {-a.x, -a.y}; }
-    friend constexpr Vec2 operator*(T s, Vec2 a) { return {s * a.x, s * a.y}; }
-    friend constexpr Vec2 operator*(Vec2 a, T s) { return {s * a.x, s * a.y}; }
-    friend constexpr Vec2 operator/(Vec2 a, T s) { return {a.x / s, a.y / s}; }
-};
-
-template <typename T> struct Vec3 {
-    T x{}, y{}, z{};
-    constexpr bool operator==(const Vec3&) const = default;
-    friend constexpr Vec3 operator+(Vec3 a, Vec3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
-    friend constexpr Vec3 operator-(Vec3 a, Vec3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
-    friend constexpr Vec3 operator-(Vec3 a) { return {-a.x, -a.y, -a.z}; }
-    friend constexpr Vec3 operator*(T s, Vec3 a) { return {s * a.x, s * a.y, s * a.z}; }
-    friend constexpr Vec3 operator*(Vec3 a, T s) { return {s * a.x, s * a.y, s * a.z}; }
-    friend constexpr Vec3 operator/(Vec3 a, T s) { return {a.x / s, a.y / s, a.z / s}; }
-    constexpr Vec2<T> xy() const { return {x, y}; }
-};
-
-template <typename T> constexpr T dot(Vec2<T> a, Vec2<T> b) { return a.x * b.x + a.y * b.y; }
-template <typename T> constexpr T cross(Vec2<T> a, Vec2<T> b) { return a.x * b.y - a.y * b.x; }
-template <typename T> constexpr T dot(Vec3<T> a, Vec3<T> b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
-template <typename T> constexpr Vec3<T> cross(Vec3<T> a, Vec3<T> b) {
-    return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
-}
-template <typename T> constexpr T squared_norm(Vec2<T> a) { return dot(a, a); }
-template <typename T> constexpr T squared_norm(Vec3<T> a) { return dot(a, a); }
-template <typename T> T norm(Vec2<T> a) { return std::sqrt(dot(a, a)); }
-template <typename T> T norm(Vec3<T> a) { return std::sqrt(dot(a, a)); }
-template <typename T> constexpr Vec2<T> perp(Vec2<T> a) { return {-a.y, a.x}; }
-template <class V> V normalized(V a) {
-    const auto n = norm(a);
-    if (!(n > 0)) throw std::domain_error("cannot normalize zero vector");
-    return a / n;
-}
-
-// Row-major 3x3 matrix.
-template <typename T> struct Mat3 {
-    std::array<T, 9> m{};
-    constexpr T& operator()(int r, int c) { return m[3 * r + c]; }
-    constexpr T operator()(int r, int c) const { return m[3 * r + c]; }
-    constexpr Vec3<T> row(int r) const { return {m[3 * r], m[3 * r + 1], m[3 * r + 2]}; }
-    constexpr Vec3<T> col(int c) const { return {m[c], m[c + 3], m[c + 6]}; }
-    static constexpr Mat3 from_rows(Vec3<T> a, Vec3<T> b, Vec3<T> c) {
-        return {{a.x, a.y, a.z, b.x, b.y, b.z, c.x, c.y, c.z}};
-    }
-    static constexpr Mat3 identity() { return {{1, 0, 0, 0, 1, 0, 0, 0, 1}}; }
-    friend constexpr Vec3<T> operator*(const Mat3& A, Vec3<T> v) {
-        return {dot(A.row(0), v), dot(A.row(1), v), dot(A.row(2), v)};
-    }
-    constexpr Mat3 transposed() const { return {{m[0], m[3], m[6], m[1], m[4], m[7], m[2], m[5], m[8]}}; }
-    constexpr T det() const { return dot(row(0), cross(row(1), row(2))); }
-};
-
-using Vec2d = Vec2<double>;
-using Vec3d = Vec3<double>;
-using Mat3d = Mat3<double>;
 
 // ---- geometry (geometry.hpp) -------------------------------------------------
 struct VolumeGeometry {
@@ -208,6 +150,31 @@ struct CutVolumeRecord {
     double volume = 0.0;
     double inv_r2 = 0.0;
 };
+
+// Introspection (cvp.hpp:24-79): the cut of a voxel base by one detector
+// column's boundary pre-images, and the z split of a vertical segment over
+// detector rows (plain and elevation-corrected).
+struct ColumnCut {
+    int column = 0;
+    Polygon2D polygon;
+    double area = 0.0;
+    Vec2d centroid{};
+};
+
+struct RowSegment {
+    int row = 0;
+    double length = 0.0;
+};
+
+std::vector<ColumnCut> column_cuts(const ViewGeometry& view, const DetectorGeometry& det,
+                                   const Polygon2D& voxel_base);
+std::vector<RowSegment> row_breakpoints(const ViewGeometry& view, const DetectorGeometry& det,
+                                        const Vec2d& centroid, double z_lo, double z_hi);
+inline double cut_volume(const ColumnCut& cut, double d) { return cut.area * d; }
+std::vector<RowSegment> elevation_corrected_split(const ViewGeometry& view,
+                                                  const DetectorGeometry& det,
+                                                  const ColumnCut& cut, double z_lo, double z_hi,
+                                                  double elevation);
 
 double pixel_scale_cos(const ViewGeometry& view, const DetectorGeometry& det, int m, int n);
 double spherical_quad_area(const Vec3d& t0, const Vec3d& t1, const Vec3d& t2, const Vec3d& t3);

@@ -362,7 +362,13 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     L.view_begin = view_begin;
     L.view_count = view_count;
     L.forward = forward ? 1 : 0;
-    L.exact = opts->precision == CVPB_PRECISION_EXACT ? 1 : 0;
+    // Both precisions form the world-scale column quantities (depth, chi1,
+    // the chi2 anchor) in float64 and run the voxel loop in offset-stable
+    // float32: that is what holds the 1e-5 bar for relaxed too (float32
+    // world coordinates — the reference's Single semantics — miss it by 6x at
+    // c3 on a noise-like stack, tests/test_config_parity_gpu.py).
+    L.exact = 1;
+    L.relaxed = opts->precision == CVPB_PRECISION_RELAXED ? 1 : 0;
     L.elevation_correction = opts->elevation_correction ? 1 : 0;
     L.cut_centroid = opts->r_estimate == CVPB_R_CUT_CENTROID ? 1 : 0;
     L.accumulate = accumulate;
@@ -398,7 +404,7 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     // to 24 of this launch's views, written into this launch's own output,
     // which the real launch then overwrites)
     // (CVPB_CVP_SHAPE=0 / 1 forces a shape, e.g. for tests)
-    const int shape_key = (L.forward << 3) | (L.exact << 2) | (L.elevation_correction << 1) | L.cut_centroid;
+    const int shape_key = (L.forward << 3) | (L.relaxed << 2) | (L.elevation_correction << 1) | L.cut_centroid;
     auto it = ctx->cvp_shape.find(shape_key);
     int shape = it != ctx->cvp_shape.end() ? it->second : 0;
     const char* forced = std::getenv("CVPB_CVP_SHAPE");
@@ -469,7 +475,7 @@ int prepare_cut_table(cvpb_context* ctx, const cvpb_cvp_options* opts, int view_
     L.views = ctx->d_views.p;
     L.view_begin = view_begin;
     L.view_count = view_count;
-    L.exact = opts->precision == CVPB_PRECISION_EXACT ? 1 : 0;
+    L.exact = 1;  // both precisions: float64 world quantities (see run_cvp)
     L.elevation_correction = opts->elevation_correction ? 1 : 0;
     L.err = ctx->d_err.p;
     auto& key = ctx->cut_key;
@@ -1092,7 +1098,7 @@ int cvpb_collect_cut_records(cvpb_context* ctx, const cvpb_cvp_options* opts, in
     double* d_vol = ctx->d_rec_d.p;
     double* d_inv = d_vol + cap;
     CVPB_CUDA(cvpb::launch_cut_records(ctx->sc, ctx->d_views.p, view, i, j, k,
-                                       opts->precision == CVPB_PRECISION_EXACT,
+                                       1,  // float64 world quantities in both precisions
                                        opts->elevation_correction,
                                        opts->r_estimate == CVPB_R_CUT_CENTROID, clamp, cap, d_rows,
                                        d_cols, d_vol, d_inv, d_n, ctx->d_err.p, st));

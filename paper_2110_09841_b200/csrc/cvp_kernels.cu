@@ -796,10 +796,8 @@ cudaError_t run_cut_table(const Scene& sc, const ViewConst* views, const CutTabl
                           int corr, int* err, cudaStream_t stream) {
     const size_t total = size_t(t.ncols) * t.nv;
     const int blocks = int(std::min<size_t>((total + 255) / 256, 148 * 64));
-    if (exact)
-        cut_table_kernel<true><<<blocks, 256, 0, stream>>>(sc, views, t, corr, err);
-    else
-        cut_table_kernel<false><<<blocks, 256, 0, stream>>>(sc, views, t, corr, err);
+    (void)exact;  // float64 world quantities in both precisions (api.cpp run_cvp)
+    cut_table_kernel<true><<<blocks, 256, 0, stream>>>(sc, views, t, corr, err);
     return cudaGetLastError();
 }
 
@@ -940,10 +938,9 @@ cudaError_t CVP_PUB(launch_cvp)(const CvpLaunch& L, cudaStream_t stream) {
             if (e != cudaSuccess) return e;
         }
         dim3 grid(nbricks, groups);
-        e = L.forward ? (L.exact ? launch_opts<true, true>(p, grid, dyn, L.tall_voxels, stream)
-                                 : launch_opts<false, true>(p, grid, dyn, L.tall_voxels, stream))
-                      : (L.exact ? launch_opts<true, false>(p, grid, dyn, L.tall_voxels, stream)
-                                 : launch_opts<false, false>(p, grid, dyn, L.tall_voxels, stream));
+        // (float64 world quantities in both precisions: EXACT geometry always)
+        e = L.forward ? launch_opts<true, true>(p, grid, dyn, L.tall_voxels, stream)
+                      : launch_opts<true, false>(p, grid, dyn, L.tall_voxels, stream);
         if (e != cudaSuccess) return e;
         if (!L.forward && last && L.vol_out64 && !p.vol_out64) {
             e = launch_f32_to_f64(L.vol_out, L.vol_out64, nvox, stream);
@@ -981,12 +978,9 @@ cudaError_t launch_cut_records(const Scene& sc, const ViewConst* views, int view
                                int k, int exact, int corr, int per_row_r, int clamp, int cap,
                                int* rows, int* cols, double* vol, double* inv, int* n_out, int* err,
                                cudaStream_t stream) {
-    if (exact)
-        cut_records_kernel<true><<<1, 1, 0, stream>>>(sc, views, view, i, j, k, corr, per_row_r,
-                                                      clamp, cap, rows, cols, vol, inv, n_out, err);
-    else
-        cut_records_kernel<false><<<1, 1, 0, stream>>>(sc, views, view, i, j, k, corr, per_row_r,
-                                                       clamp, cap, rows, cols, vol, inv, n_out, err);
+    (void)exact;
+    cut_records_kernel<true><<<1, 1, 0, stream>>>(sc, views, view, i, j, k, corr, per_row_r, clamp,
+                                                  cap, rows, cols, vol, inv, n_out, err);
     return cudaGetLastError();
 }
 #endif  // shape-independent entry points

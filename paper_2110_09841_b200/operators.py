@@ -36,7 +36,7 @@ class PixelScaling(enum.IntEnum):
 
 class CvpPrecision(enum.IntEnum):
     Double = 0   # exact: float64 cut geometry + float64 voxel anchors
-    Single = 1   # relaxed: float32 throughout (reference Single semantics)
+    Single = 1   # relaxed (same float64 column geometry)
 
 
 class RadiusEstimate(enum.IntEnum):
