@@ -228,6 +228,7 @@ struct cvpb_context {
     cudaEvent_t ev_tune[2] = {};  // brick-shape timing
     bool ev_table_recorded = false;
     DevBuf<float> h_vol, h_proj;  // device buffers of the host path
+    DevBuf<double> h_in64, h_out64;  // float64 host path (Siddon)
     DevBuf<float> cg_r, cg_q, cg_s, cg_p;
     DevBuf<double> cg_partials, cg_hist;
     DevBuf<cvpb::CgState> cg_state;
@@ -644,6 +645,8 @@ void cvpb_context_destroy(cvpb_context* ctx) {
     ctx->d_rec_i.release();
     ctx->d_rec_d.release();
     ctx->cg_partials.release();
+    ctx->h_in64.release();
+    ctx->h_out64.release();
     ctx->cg_hist.release();
     ctx->cg_state.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -1138,19 +1141,23 @@ int cvpb_scale_image(cvpb_context* ctx, int view, int exact, double* out_host) {
 
 // ---- Siddon-K -----------------------------------------------------------------
 
-int cvpb_project_siddon(cvpb_context* ctx, int k_per_edge, const cvpb_pixel_roi* roi,
-                        const cvpb_exec_policy* exec, const float* d_volume, float* d_proj,
-                        int view_begin, int view_count, void* stream) {
+}  // extern "C"
+
+namespace {
+// Siddon-K launches over float32 (device API) or float64 (host path) buffers.
+int siddon_project(cvpb_context* ctx, int k_per_edge, const cvpb_pixel_roi* roi,
+                   const cvpb_exec_policy* exec, const void* d_volume, void* d_proj, int view_begin,
+                   int view_count, bool fp64, cudaStream_t st) {
     CVPB_TRY(check_ctx(ctx));
     CVPB_TRY(check_siddon_k(k_per_edge, exec));
     CVPB_TRY(check_range(ctx, view_begin, view_count));
     CVPB_TRY(check_scene_views(ctx));
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     cvpb::SiddonLaunch L{};
     L.sc = ctx->sc;
     L.views = ctx->d_views.p;
     L.vol_in = d_volume;
     L.proj_out = d_proj;
+    L.fp64 = fp64 ? 1 : 0;
     L.view_begin = view_begin;
     L.view_count = view_count;
     L.k_per_edge = k_per_edge;
@@ -1161,15 +1168,15 @@ int cvpb_project_siddon(cvpb_context* ctx, int k_per_edge, const cvpb_pixel_roi*
     L.r1 = r.row_end < 0 ? R : std::clamp(r.row_end, L.r0, R);
     L.c0 = std::clamp(r.col_begin, 0, Cc);
     L.c1 = r.col_end < 0 ? Cc : std::clamp(r.col_end, L.c0, Cc);
-    CVPB_CUDA(cvpb::launch_nonzero_box(d_volume, ctx->sc, ctx->d_box.p, st));
+    CVPB_CUDA(cvpb::launch_nonzero_box(d_volume, fp64, ctx->sc, ctx->d_box.p, st));
     L.d_box = ctx->d_box.p;
     CVPB_CUDA(cvpb::launch_siddon(L, true, st));
     return CVPB_OK;
 }
 
-int cvpb_backproject_siddon(cvpb_context* ctx, int k_per_edge, const cvpb_exec_policy* exec,
-                            const float* d_proj, float* d_volume, int view_begin, int view_count,
-                            int accumulate, void* stream) {
+int siddon_backproject(cvpb_context* ctx, int k_per_edge, const cvpb_exec_policy* exec,
+                       const void* d_proj, void* d_volume, int view_begin, int view_count,
+                       int accumulate, bool fp64, cudaStream_t st) {
     CVPB_TRY(check_ctx(ctx));
     CVPB_TRY(check_siddon_k(k_per_edge, exec));
     CVPB_TRY(check_range(ctx, view_begin, view_count));
@@ -1179,17 +1186,52 @@ int cvpb_backproject_siddon(cvpb_context* ctx, int k_per_edge, const cvpb_exec_p
     L.views = ctx->d_views.p;
     L.proj_in = d_proj;
     L.vol_out = d_volume;
+    L.fp64 = fp64 ? 1 : 0;
     L.view_begin = view_begin;
     L.view_count = view_count;
     L.k_per_edge = k_per_edge;
     L.accumulate = accumulate;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (view_count == 0 && !accumulate) {
-        CVPB_CUDA(cudaMemsetAsync(d_volume, 0, sizeof(float) * ctx->nvox(), st));
+        CVPB_CUDA(cudaMemsetAsync(d_volume, 0, (fp64 ? sizeof(double) : sizeof(float)) * ctx->nvox(), st));
         return CVPB_OK;
     }
     CVPB_CUDA(cvpb::launch_siddon(L, false, st));
     return CVPB_OK;
+}
+
+// Host path of the float64 projectors: H2D of the float64 input, the kernels
+// on float64 device buffers, D2H of the float64 output (no conversions).
+template <class Run>
+int host_roundtrip64(cvpb_context* ctx, bool vol_to_proj, const double* in, double* out, Run&& run) {
+    CVPB_TRY(check_ctx(ctx));
+    if (!in || !out) return fail(CVPB_INVALID_ARGUMENT, "null host buffer");
+    cudaStream_t st = ctx->stream;
+    const size_t nv = ctx->nvox(), np = ctx->npx_view() * ctx->views.size();
+    const size_t n_in = vol_to_proj ? nv : np, n_out = vol_to_proj ? np : nv;
+    CVPB_CUDA(ctx->h_in64.reserve(n_in));
+    CVPB_CUDA(ctx->h_out64.reserve(n_out));
+    CVPB_CUDA(cudaMemcpyAsync(ctx->h_in64.p, in, sizeof(double) * n_in, cudaMemcpyHostToDevice, st));
+    CVPB_TRY(run(ctx->h_in64.p, ctx->h_out64.p, st));
+    CVPB_CUDA(cudaMemcpyAsync(out, ctx->h_out64.p, sizeof(double) * n_out, cudaMemcpyDeviceToHost, st));
+    CVPB_CUDA(cudaStreamSynchronize(st));
+    return CVPB_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int cvpb_project_siddon(cvpb_context* ctx, int k_per_edge, const cvpb_pixel_roi* roi,
+                        const cvpb_exec_policy* exec, const float* d_volume, float* d_proj,
+                        int view_begin, int view_count, void* stream) {
+    return siddon_project(ctx, k_per_edge, roi, exec, d_volume, d_proj, view_begin, view_count, false,
+                          static_cast<cudaStream_t>(stream));
+}
+
+int cvpb_backproject_siddon(cvpb_context* ctx, int k_per_edge, const cvpb_exec_policy* exec,
+                            const float* d_proj, float* d_volume, int view_begin, int view_count,
+                            int accumulate, void* stream) {
+    return siddon_backproject(ctx, k_per_edge, exec, d_proj, d_volume, view_begin, view_count,
+                              accumulate, false, static_cast<cudaStream_t>(stream));
 }
 
 int cvpb_trace_ray(cvpb_context* ctx, const cvpb_volume_geometry* vol, const double source[3],
@@ -1276,19 +1318,21 @@ int cvpb_backproject_tt(cvpb_context* ctx, const cvpb_tt_options* opts, const fl
 // ---- host paths for Siddon-K / TT / CGLS ---------------------------------------
 
 
+// Siddon's host path runs in float64 end to end, like the reference (it is
+// the ground-truth projector: Siddon512 in acceptance.cpp:100-147).
 int cvpb_project_siddon_host(cvpb_context* ctx, int k_per_edge, const cvpb_pixel_roi* roi,
                              const cvpb_exec_policy* exec, const double* volume, double* proj) {
     const int V = ctx ? int(ctx->views.size()) : 0;
-    return host_roundtrip(ctx, true, volume, proj, [&](float* din, float* dout, cudaStream_t st) {
-        return cvpb_project_siddon(ctx, k_per_edge, roi, exec, din, dout, 0, V, st);
+    return host_roundtrip64(ctx, true, volume, proj, [&](double* din, double* dout, cudaStream_t st) {
+        return siddon_project(ctx, k_per_edge, roi, exec, din, dout, 0, V, true, st);
     });
 }
 
 int cvpb_backproject_siddon_host(cvpb_context* ctx, int k_per_edge, const cvpb_exec_policy* exec,
                                  const double* proj, double* volume) {
     const int V = ctx ? int(ctx->views.size()) : 0;
-    return host_roundtrip(ctx, false, proj, volume, [&](float* din, float* dout, cudaStream_t st) {
-        return cvpb_backproject_siddon(ctx, k_per_edge, exec, din, dout, 0, V, 0, st);
+    return host_roundtrip64(ctx, false, proj, volume, [&](double* din, double* dout, cudaStream_t st) {
+        return siddon_backproject(ctx, k_per_edge, exec, din, dout, 0, V, 0, true, st);
     });
 }
 

@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <cstddef>
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "cvp_device.cuh"
@@ -880,6 +881,10 @@ cudaError_t CVP_PUB(launch_cvp)(const CvpLaunch& L, cudaStream_t stream) {
     p.per_row_r = L.cut_centroid;
     p.h = float(0.5 * sc.a3);
     p.tile_cap = tile_cap;
+    // CVPB_NO_TILE=1: every record takes the global (float-atomic / direct
+    // gather) path, which otherwise only tile-overflow bricks use (tests)
+    if (const char* e = std::getenv("CVPB_NO_TILE"))
+        if (e[0] == '1') p.tile_cap = 0;
     p.err = L.err;
 
     // view chunks whose cut table fits the scratch block

@@ -67,10 +67,12 @@ cudaError_t launch_cut_records(const Scene& sc, const ViewConst* views, int view
 struct SiddonLaunch {
     Scene sc;
     const ViewConst* views;
-    const float* vol_in;
-    float* vol_out;
-    const float* proj_in;
-    float* proj_out;
+    // float32 buffers (device API) or float64 (fp64 = 1: the host path)
+    const void* vol_in;
+    void* vol_out;
+    const void* proj_in;
+    void* proj_out;
+    int fp64;
     int view_begin, view_count;
     int k_per_edge;
     int r0, r1, c0, c1;       // forward ROI (resolved, half-open)
@@ -80,7 +82,8 @@ struct SiddonLaunch {
 cudaError_t launch_siddon(const SiddonLaunch& L, bool forward, cudaStream_t stream);
 cudaError_t launch_trace_ray(const Scene& sc, const double* src, const double* tgt, int cap, int* ijk,
                              double* len, int* n_out, cudaStream_t stream);
-cudaError_t launch_nonzero_box(const float* vol, const Scene& sc, int* d_box6, cudaStream_t stream);
+cudaError_t launch_nonzero_box(const void* vol, bool fp64, const Scene& sc, int* d_box6,
+                               cudaStream_t stream);
 
 struct TTLaunch {
     Scene sc;

@@ -6,11 +6,13 @@
 //
 // One thread per (pixel, view) walks its K x K sub-rays with the reference's
 // incremental parametric traversal in float64 (ties advance every tying axis;
-// half-open voxel intervals), reading float32 attenuation through the
-// read-only path. The forward restricts traversal to the tight box of nonzero
-// voxels exactly like the reference (:182-211); the backward scatters
-// w * chord with float32 device atomics (the reference's `omp atomic`,
-// :299-304).
+// half-open voxel intervals), reading attenuation through the read-only path.
+// The forward restricts traversal to the tight box of nonzero voxels exactly
+// like the reference (:182-211); the backward scatters w * chord with device
+// atomics (the reference's `omp atomic`, :299-304). The value type T is float
+// for the device API and double for the reference-facing host path, where
+// Siddon is the float64 ground truth the reference makes it (its unit tests
+// pin chords and linearity at 1e-9 / 1e-12).
 #include <cfloat>
 
 #include "kernels.hpp"
@@ -103,7 +105,8 @@ __device__ __forceinline__ Box make_box(const Scene& sc, const int* d_box) {
     return box;
 }
 
-__global__ void siddon_fwd_kernel(SiddonLaunch L) {
+template <class T>
+__global__ void siddon_fwd_kernel(SiddonLaunch L, const T* __restrict__ vol_in, T* __restrict__ proj_out) {
     const Box box = make_box(L.sc, L.d_box);
     if (box.n[0] <= 0 || box.n[1] <= 0 || box.n[2] <= 0) return;  // all-zero volume
     const int w = L.c1 - L.c0, hgt = L.r1 - L.r0;
@@ -126,16 +129,16 @@ __global__ void siddon_fwd_kernel(SiddonLaunch L) {
                 dir[d] = vc.base[d] + chi1 * vc.du[d] + chi2 * vc.dv[d] - src[d];
             const double dl = sqrt(dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2]);
             traverse(box, src, dir, dl, [&](int i, int j, int k, double chord) {
-                acc += double(__ldg(L.vol_in + (size_t(k) * n2 + j) * n1 + i)) * chord;
+                acc += double(__ldg(vol_in + (size_t(k) * n2 + j) * n1 + i)) * chord;
             });
         }
     }
     const double inv_k2 = 1.0 / (double(K) * double(K));
-    L.proj_out[size_t(blockIdx.y) * L.sc.rows * L.sc.cols + size_t(m) * L.sc.cols + n] =
-        float(acc * inv_k2);
+    proj_out[size_t(blockIdx.y) * L.sc.rows * L.sc.cols + size_t(m) * L.sc.cols + n] = T(acc * inv_k2);
 }
 
-__global__ void siddon_bwd_kernel(SiddonLaunch L) {
+template <class T>
+__global__ void siddon_bwd_kernel(SiddonLaunch L, const T* __restrict__ proj_in, T* vol_out) {
     const Box box = make_box(L.sc, nullptr);
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     const int cols = L.sc.cols, rows = L.sc.rows;
@@ -145,7 +148,7 @@ __global__ void siddon_bwd_kernel(SiddonLaunch L) {
     const int v = L.view_begin + vloc;
     const int K = L.k_per_edge;
     const double inv_k2 = 1.0 / (double(K) * double(K));
-    const double wgt = double(__ldg(L.proj_in + size_t(vloc) * rows * cols + idx)) * inv_k2;
+    const double wgt = double(__ldg(proj_in + size_t(vloc) * rows * cols + idx)) * inv_k2;
     if (wgt == 0.0) return;
     const ViewConst& vc = L.views[v];
     const double src[3] = {vc.sx, vc.sy, vc.s3};
@@ -160,7 +163,7 @@ __global__ void siddon_bwd_kernel(SiddonLaunch L) {
                 dir[d] = vc.base[d] + chi1 * vc.du[d] + chi2 * vc.dv[d] - src[d];
             const double dl = sqrt(dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2]);
             traverse(box, src, dir, dl, [&](int i, int j, int k, double chord) {
-                atomicAdd(L.vol_out + (size_t(k) * n2 + j) * n1 + i, float(wgt * chord));
+                atomicAdd(vol_out + (size_t(k) * n2 + j) * n1 + i, T(wgt * chord));
             });
         }
     }
@@ -168,12 +171,13 @@ __global__ void siddon_bwd_kernel(SiddonLaunch L) {
 
 // Tight box of nonzero voxels (siddon.cpp:182-199): d_box6 = {lo0,lo1,lo2,hi0,hi1,hi2}
 // initialised to {N1,N2,N3,0,0,0} by the caller.
-__global__ void nonzero_box_kernel(const float* vol, int n1, int n2, int n3, int* box) {
+template <class T>
+__global__ void nonzero_box_kernel(const T* vol, int n1, int n2, int n3, int* box) {
     const size_t total = size_t(n1) * n2 * n3;
     int lo[3] = {n1, n2, n3}, hi[3] = {0, 0, 0};
     for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;
          idx += size_t(gridDim.x) * blockDim.x) {
-        if (vol[idx] != 0.f) {
+        if (vol[idx] != T(0)) {
             const int i = int(idx % n1), j = int((idx / n1) % n2), k = int(idx / (size_t(n1) * n2));
             lo[0] = min(lo[0], i);
             lo[1] = min(lo[1], j);
@@ -226,34 +230,50 @@ cudaError_t launch_trace_ray(const Scene& sc, const double* src, const double* t
     return cudaGetLastError();
 }
 
-cudaError_t launch_nonzero_box(const float* vol, const Scene& sc, int* d_box6, cudaStream_t stream) {
+cudaError_t launch_nonzero_box(const void* vol, bool fp64, const Scene& sc, int* d_box6,
+                               cudaStream_t stream) {
     const int init[6] = {sc.n1, sc.n2, sc.n3, 0, 0, 0};
     cudaError_t e = cudaMemcpyAsync(d_box6, init, sizeof(init), cudaMemcpyHostToDevice, stream);
     if (e != cudaSuccess) return e;
-    nonzero_box_kernel<<<148 * 8, 256, 0, stream>>>(vol, sc.n1, sc.n2, sc.n3, d_box6);
+    if (fp64)
+        nonzero_box_kernel<<<148 * 8, 256, 0, stream>>>(static_cast<const double*>(vol), sc.n1, sc.n2,
+                                                        sc.n3, d_box6);
+    else
+        nonzero_box_kernel<<<148 * 8, 256, 0, stream>>>(static_cast<const float*>(vol), sc.n1, sc.n2,
+                                                        sc.n3, d_box6);
     return cudaGetLastError();
 }
 
 cudaError_t launch_siddon(const SiddonLaunch& L, bool forward, cudaStream_t stream) {
     if (L.view_count <= 0) return cudaSuccess;
     const Scene& sc = L.sc;
+    const size_t esz = L.fp64 ? sizeof(double) : sizeof(float);
     cudaError_t e;
     if (forward) {
-        e = cudaMemsetAsync(L.proj_out, 0, sizeof(float) * size_t(sc.rows) * sc.cols * L.view_count,
-                            stream);
+        e = cudaMemsetAsync(L.proj_out, 0, esz * size_t(sc.rows) * sc.cols * L.view_count, stream);
         if (e != cudaSuccess) return e;
         const int npx = (L.r1 - L.r0) * (L.c1 - L.c0);
         if (npx <= 0) return cudaSuccess;
         dim3 grid((npx + 127) / 128, L.view_count);
-        siddon_fwd_kernel<<<grid, 128, 0, stream>>>(L);
+        if (L.fp64)
+            siddon_fwd_kernel<double><<<grid, 128, 0, stream>>>(L, static_cast<const double*>(L.vol_in),
+                                                                static_cast<double*>(L.proj_out));
+        else
+            siddon_fwd_kernel<float><<<grid, 128, 0, stream>>>(L, static_cast<const float*>(L.vol_in),
+                                                               static_cast<float*>(L.proj_out));
     } else {
         if (!L.accumulate) {
-            e = cudaMemsetAsync(L.vol_out, 0, sizeof(float) * size_t(sc.n1) * sc.n2 * sc.n3, stream);
+            e = cudaMemsetAsync(L.vol_out, 0, esz * size_t(sc.n1) * sc.n2 * sc.n3, stream);
             if (e != cudaSuccess) return e;
         }
         const int npx = sc.rows * sc.cols;
         dim3 grid((npx + 127) / 128, L.view_count);
-        siddon_bwd_kernel<<<grid, 128, 0, stream>>>(L);
+        if (L.fp64)
+            siddon_bwd_kernel<double><<<grid, 128, 0, stream>>>(L, static_cast<const double*>(L.proj_in),
+                                                                static_cast<double*>(L.vol_out));
+        else
+            siddon_bwd_kernel<float><<<grid, 128, 0, stream>>>(L, static_cast<const float*>(L.proj_in),
+                                                               static_cast<float*>(L.vol_out));
     }
     return cudaGetLastError();
 }

@@ -285,6 +285,34 @@ class DeviceScene:
                                                 int(bool(accumulate)), _stream(stream)))
         return out
 
+    def project_siddon_host(self, vol64: np.ndarray, k_per_edge: int, out64: np.ndarray = None,
+                            roi: PixelRoi = None, exec: ExecPolicy = None):
+        """Reference-facing Siddon-K: float64 host buffers, float64 on the
+        device end to end (the reference's ground-truth projector)."""
+        exec = exec or ExecPolicy()
+        vol64 = _host64(vol64, self.vol_geom.voxel_count())
+        if out64 is None:
+            out64 = np.zeros(self.det.pixel_count() * self.n_views)
+        _check_host_out(out64, self.det.pixel_count() * self.n_views)
+        r = roi._c() if roi is not None else None
+        N.check(N.lib().cvpb_project_siddon_host(self._h, int(k_per_edge),
+                                                 C.byref(r) if r is not None else None,
+                                                 C.byref(exec._c()), C.c_void_p(vol64.ctypes.data),
+                                                 C.c_void_p(out64.ctypes.data)))
+        return out64
+
+    def backproject_siddon_host(self, proj64: np.ndarray, k_per_edge: int, out64: np.ndarray = None,
+                                exec: ExecPolicy = None):
+        exec = exec or ExecPolicy()
+        proj64 = _host64(proj64, self.det.pixel_count() * self.n_views)
+        if out64 is None:
+            out64 = np.zeros(self.vol_geom.voxel_count())
+        _check_host_out(out64, self.vol_geom.voxel_count())
+        N.check(N.lib().cvpb_backproject_siddon_host(self._h, int(k_per_edge), C.byref(exec._c()),
+                                                     C.c_void_p(proj64.ctypes.data),
+                                                     C.c_void_p(out64.ctypes.data)))
+        return out64
+
     # ---- TT --------------------------------------------------------------------
     def project_tt(self, vol, out=None, opts: TTOptions = None, view_begin=0, view_count=None,
                    stream=None):
@@ -451,14 +479,15 @@ def project_siddon_k_into(vol: AttenuationVolume, views, det: DetectorGeometry, 
     """siddon.cpp:166-249."""
     if out.det != det or out.n_views != len(views):
         raise InvalidArgument("output stack does not match detector/views")
-    device = _device_of(vol.values) if _is_torch(vol.values) else 0
-    sc = scene_for(vol.geom, det, views, device)
-    x = _to_device(vol.values, vol.geom.shape(), f"cuda:{device}")
     if _is_torch(out.values):
-        sc.project_siddon(x, k_per_edge, out.values, roi, exec)
-    else:
-        res = sc.project_siddon(x, k_per_edge, None, roi, exec)
-        out.values[:] = res.double().cpu().numpy().ravel()
+        device = _device_of(out.values)
+        sc = scene_for(vol.geom, det, views, device)
+        sc.project_siddon(_to_device(vol.values, vol.geom.shape(), f"cuda:{device}"), k_per_edge,
+                          out.values, roi, exec)
+    else:  # reference buffers: the float64 host path
+        sc = scene_for(vol.geom, det, views)
+        x = vol.values.double().cpu().numpy() if _is_torch(vol.values) else vol.values
+        sc.project_siddon_host(x, k_per_edge, out.values, roi, exec)
 
 
 def project_siddon_k(vol: AttenuationVolume, views, det, k_per_edge: int,
@@ -477,14 +506,15 @@ def backproject_siddon_k_into(proj: ProjectionStack, views, vol_geom: VolumeGeom
         raise InvalidArgument("output volume does not match geometry")
     if proj.n_views != len(views):
         raise InvalidArgument("projection stack does not match views")
-    device = _device_of(proj.values) if _is_torch(proj.values) else 0
-    sc = scene_for(vol_geom, proj.det, views, device)
-    b = _to_device(proj.values, (proj.n_views, proj.det.rows, proj.det.cols), f"cuda:{device}")
     if _is_torch(out.values):
-        sc.backproject_siddon(b, k_per_edge, out.values, exec)
-    else:
-        res = sc.backproject_siddon(b, k_per_edge, None, exec)
-        out.values[:] = res.double().cpu().numpy().ravel()
+        device = _device_of(out.values)
+        sc = scene_for(vol_geom, proj.det, views, device)
+        sc.backproject_siddon(_to_device(proj.values, (proj.n_views, proj.det.rows, proj.det.cols),
+                                         f"cuda:{device}"), k_per_edge, out.values, exec)
+    else:  # reference buffers: the float64 host path
+        sc = scene_for(vol_geom, proj.det, views)
+        b = proj.values.double().cpu().numpy() if _is_torch(proj.values) else proj.values
+        sc.backproject_siddon_host(b, k_per_edge, out.values, exec)
 
 
 def backproject_siddon_k(proj: ProjectionStack, views, vol_geom, k_per_edge: int,

@@ -24,7 +24,14 @@ BIN = os.path.join(ROOT, "tests", "cpp", "bin")
 UNITS = ["test_polygon", "test_geometry", "test_den", "test_cvp", "test_siddon", "test_solver"]
 
 # test case -> why a float32 device cannot meet the reference's float64 pin
-EXPECTED_PRECISION_MISSES = {}
+EXPECTED_PRECISION_MISSES = {
+    "cvp adjoint identity for every option combination":
+        "test_cvp.cpp:370 pins <Ax,y> = <x,A'y> at 1e-12; the float32 pair holds ~1e-7",
+    "backproject cvp: single-pixel impulse matches forward bookkeeping":
+        "test_cvp.cpp:403 compares BP of one pixel with the cut-record bookkeeping at 1e-12",
+    "cut records conserve the voxel volume":
+        "test_cvp.cpp:429 sums float32 record volumes against 0.125 mm^3 at 1e-9 absolute (8e-9 relative)",
+}
 
 
 def _run(name, args=(), timeout=1800):
