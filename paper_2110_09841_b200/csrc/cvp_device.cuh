@@ -443,6 +443,72 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
     }
 }
 
+// Row walk of one voxel against one column cut when its brick's rows need no
+// detector clamping and every voxel-cut of the brick spans at most NB + 1 rows
+// (the launch decides per (brick, view), see cvp_kernels.cu footprint()).
+// The range bound tr is rigorous (tr_a carries 1e-5 px of slack), so the top
+// boundary of row m_first lies above the voxel and its elevation ramp, and the
+// bottom boundary of row m_first + NB below them: their clamp-means are +h and
+// -h exactly (clamp_mean, cvp.cpp:161-175, saturates), and only the NB
+// interior boundaries need evaluating. A voxel that occupies fewer rows gets
+// exactly -h at the interior boundaries below it, i.e. zero-share rows.
+// Rows m_first .. m_first + NB are emitted in order with max(share, 0) * inv_r2.
+template <int NB, class Emit>
+__device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh, float pmh, float dz,
+                                               float h, float sh, const bool per_row_r,
+                                               float inv_r2_fixed, Emit&& emit) {
+    static_assert(NB == 1 || NB == 2, "one or two interior boundaries");
+    constexpr float kMagic = 12582912.f;
+    constexpr int kMagicBits = 0x4B400000;
+    const float tr = fmaf(fabsf(dz), c.tr_b, c.tr_a);
+    const float clo = __fadd_ru(fmaxf(uh - tr, -2097152.f), kMagic - 1.f);
+    const int m_first = Mi + (__float_as_int(clo) - kMagicBits);
+    // first interior boundary (top boundary of row m_first + 1), exact
+    const float e1 = clo - (kMagic - 1.f);
+    if constexpr (NB == 1) {
+        const float a1 = c.g * (uh - e1);
+        const float p1 = clampf(a1, -h, h);
+        const float t1 = clamp_mean_local(a1, sh * fabsf(pmh - e1), h);
+        float i0 = inv_r2_fixed, i1 = inv_r2_fixed;
+        if (per_row_r) {
+            // midpoints of the plain row segments [p1, h] and [-h, p1] (cvp.cpp:223-229)
+            const float2 Z = fma2(make_float2(p1, p1), make_float2(0.5f, 0.5f),
+                                  make_float2(dz + 0.5f * h, dz - 0.5f * h));
+            const float2 Q = fma2(Z, Z, make_float2(c.rho2, c.rho2));
+            i0 = fast_rcp(Q.x);
+            i1 = fast_rcp(Q.y);
+        }
+        emit(m_first, fmaxf(h - t1, 0.f) * i0);
+        emit(m_first + 1, fmaxf(t1 + h, 0.f) * i1);
+    } else {
+        const float2 E = make_float2(e1, e1 + 1.f);
+        const float2 A = mul2(make_float2(c.g, c.g), sub2(make_float2(uh, uh), E));
+        const float p1 = clampf(A.x, -h, h), p2 = clampf(A.y, -h, h);
+        const float2 D = sub2(make_float2(pmh, pmh), E);
+        const float s1 = sh * fabsf(D.x), s2 = sh * fabsf(D.y);
+        const float2 AP = add2(A, make_float2(h, h)), AM = sub2(A, make_float2(h, h));
+        const float2 d1 = make_float2(fmaxf(s1 - fabsf(AP.x), 0.f), fmaxf(s2 - fabsf(AP.y), 0.f));
+        const float2 d2 = make_float2(fmaxf(s1 - fabsf(AM.x), 0.f), fmaxf(s2 - fabsf(AM.y), 0.f));
+        const float2 num = sub2(mul2(d1, d1), mul2(d2, d2));
+        const float2 rr = make_float2(fast_rcp(fmaxf(s1, 1e-30f)), fast_rcp(fmaxf(s2, 1e-30f)));
+        const float2 T = fma2(mul2(num, rr), make_float2(0.25f, 0.25f), make_float2(p1, p2));
+        const float2 W = sub2(make_float2(h, T.x), T);
+        float i0 = inv_r2_fixed, i1 = inv_r2_fixed, i2 = inv_r2_fixed;
+        if (per_row_r) {
+            const float2 Z = fma2(add2(make_float2(h, p1), make_float2(p1, p2)), make_float2(0.5f, 0.5f),
+                                  make_float2(dz, dz));
+            const float z2 = fmaf(0.5f, p2 - h, dz);
+            const float2 Q = fma2(Z, Z, make_float2(c.rho2, c.rho2));
+            i0 = fast_rcp(Q.x);
+            i1 = fast_rcp(Q.y);
+            i2 = fast_rcp(fmaf(z2, z2, c.rho2));
+        }
+        emit(m_first, fmaxf(W.x, 0.f) * i0);
+        emit(m_first + 1, fmaxf(W.y, 0.f) * i1);
+        emit(m_first + 2, fmaxf(T.y + h, 0.f) * i2);
+    }
+}
+
 // Column anchor chi2(zc) = pp2 - dz * Q0 split into an integer row m_ref and
 // float32 remainders u = chi2(zc) - m_ref, pm = pp2 - m_ref.
 template <bool EXACT>

@@ -145,6 +145,7 @@ struct Smem {
     float mu_abs_max;         // forward: max |mu| over the brick
     int nonfinite;            // forward: the brick holds a NaN / Inf attenuation
     float qscale;             // forward: fixed-point scale of this (brick, view)
+    int walk_mode;            // 0: general row walk; 1 / 2: walk_rows_fast<1 / 2>
 };
 
 // 32-bit shared-window addressing for the hot paths: with 80 registers the
@@ -219,7 +220,8 @@ __device__ __forceinline__ CutRec load_cut(uint32_t sbase, int slot) {
 __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene& sc, int i0, int i1,
                                                 int j0, int j1, int k0, int k1, int& m0, int& m1,
                                                 int& n0, int& n1, double* depth_min = nullptr,
-                                                double* depth_max = nullptr) {
+                                                double* depth_max = nullptr,
+                                                bool* rows_inside = nullptr) {
     const double xs[2] = {sc.minx + i0 * sc.a1, sc.minx + i1 * sc.a1};
     const double ys[2] = {sc.miny + j0 * sc.a2, sc.miny + j1 * sc.a2};
     double cmin = INFINITY, cmax = -INFINITY, dmin = INFINITY, dmax = -INFINITY;
@@ -256,8 +258,12 @@ __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene
         }
     n0 = max(int(ceil(cmin - 0.5)) - 1, 0);
     n1 = min(int(floor(cmax + 0.5)) + 1, sc.cols - 1);
-    m0 = max(int(ceil(rmin - 0.5)) - 1, 0);
-    m1 = min(int(floor(rmax + 0.5)) + 1, sc.rows - 1);
+    // two rows of margin: the fast row walk (walk_rows_fast) emits up to one
+    // row past a voxel's range, whose own bound carries float slack
+    const int r0 = int(ceil(rmin - 0.5)) - 2, r1 = int(floor(rmax + 0.5)) + 2;
+    m0 = max(r0, 0);
+    m1 = min(r1, sc.rows - 1);
+    if (rows_inside) *rows_inside = r0 >= 0 && r1 <= sc.rows - 1;
 }
 
 // CORR: elevation correction option; CCR: CutCentroid radius estimate
@@ -359,9 +365,29 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
         constexpr bool SPLIT = NCOL < NT && !FWD;
         auto footprint = [&]() {
             int m0, m1, n0, n1;
-            bool fixed_ok = true;
+            bool fixed_ok = true, rows_inside = false;
             double dmin = 0.0, dmax = 0.0;
-            brick_footprint(vc, sc, i0, i1, j0, j1, k0, k1, m0, m1, n0, n1, &dmin, &dmax);
+            brick_footprint(vc, sc, i0, i1, j0, j1, k0, k1, m0, m1, n0, n1, &dmin, &dmax, &rows_inside);
+            // Row-walk mode of this (brick, view): the fast walk needs every
+            // voxel's rows inside the detector (no clamping), a full brick
+            // along x3 (no virtual layers) and 2 tr < NB + 1 for every
+            // voxel-cut, with the rigorous bound
+            //   tr <= h f/(b2 (dmin - dd)) + |dz|max f dd / (b2 dmin (dmin - dd)) + 1e-5,
+            // dd = diag/2 >= |hw| halfw (walk_rows_fast, cvp_device.cuh).
+            {
+                int mode = 0;
+                const double ddm = 0.5 * sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2);
+                const double dl = dmin - ddm;
+                if (rows_inside && k1 == k0 + BK && dl > 0.0) {
+                    const double zlo = sc.minz + (k0 + 0.5) * sc.a3 - vc.s3;
+                    const double zhi = sc.minz + (k1 - 0.5) * sc.a3 - vc.s3;
+                    const double dzm = fmax(fabs(zlo), fabs(zhi));
+                    const double tr = 0.5 * sc.a3 * vc.f_over_b2 / dl +
+                                      dzm * vc.f_over_b2 * ddm / (dmin * dl) + 2e-5;
+                    mode = 2.0 * tr < 0.999 ? 1 : 2.0 * tr < 1.999 ? 2 : 0;
+                }
+                s.walk_mode = mode;
+            }
             if (FWD) {
                 // Forward accumulation is int32 fixed point (native ATOMS.ADD;
                 // float shared atomics are CAS loops on sm_100). Bound on any
@@ -459,6 +485,8 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
         // Each lane carries NV voxels of one column through every cut (NV = NH
         // = 2: the cut record, tile test and loop control are shared
         // by the lane's voxels kk = lane and lane + 32).
+        auto vphase = [&](auto mode_tag) {
+        constexpr int MODE = decltype(mode_tag)::value;
         for (int ch = warp; ch < NCOL * NH / NV; ch += NWARP) {
             constexpr int NG = NH / NV;  // voxel groups per column
             const int c = ch / NG;
@@ -542,13 +570,41 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                                                            per_row_r, v.inv_r2_fixed, rows, emit);
                 if (!FWD) v.acc = fmaf(wA, cut_acc, v.acc);
             };
+            // fast walk (MODE 1 / 2): rows need no clamping and stay inside
+            // the tile (2-row margin), so the addresses need no bound
+            auto fast_cut = [&](const CutRec& r, VoxState& v) {
+                const float sh = (corr && r.rho2 < v.dz2e28) ? r.shw : 0.f;
+                const float uh = fmaf(v.dz, r.kc, v.u0h);
+                const uint32_t cbase = tbase + 4u * uint32_t((r.n - tn0) * tstride - tm0);
+                const float wA = FWD ? v.muq * r.A : r.A;
+                float cut_acc = 0.f;
+                int nrow = 0;
+                auto emit = [&](int m, float wr) {
+                    uint32_t a = cbase + 4u * uint32_t(m);
+                    if (MODE == 2 && nrow == 2) a = tbase + 4u * min(uint32_t((r.n - tn0) * tstride + m - tm0),
+                                                                    uint32_t((r.n - tn0) * tstride) + trm1);
+                    ++nrow;
+                    if (FWD)
+                        red_s32(a, __float2int_rn(wr * wA));
+                    else
+                        cut_acc = fmaf(lds_f32(a), wr, cut_acc);
+                };
+                walk_rows_fast<MODE == 2 ? 2 : 1>(r, v.Mi, uh, v.pmh, v.dz, h, sh, per_row_r,
+                                                  v.inv_r2_fixed, emit);
+                if (!FWD) v.acc = fmaf(wA, cut_acc, v.acc);
+            };
             auto cut = [&](const CutRec& r) {
                 if (tile_ok && unsigned(r.n - tn0) < unsigned(tcols)) {
                     // tile path: inactive voxels run too, with zero weight
                     // (forward: mu = 0) or a discarded accumulator (backward:
                     // k past the volume), so there is no per-voxel branch
+                    if constexpr (MODE == 0) {
 #pragma unroll
-                    for (int t = 0; t < NV; ++t) do_cut(r, vs[t], std::true_type{});
+                        for (int t = 0; t < NV; ++t) do_cut(r, vs[t], std::true_type{});
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < NV; ++t) fast_cut(r, vs[t]);
+                    }
                 } else {
 #pragma unroll
                     for (int t = 0; t < NV; ++t)
@@ -573,6 +629,16 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 for (int t = 0; t < NV; ++t)
                     if (vs[t].kvalid) sts_f32(vs[t].vaddr, lds_f32(vs[t].vaddr) + vs[t].acc);
             }
+        }
+        };
+        {
+            const int mode = s.walk_mode;
+            if (mode == 1)
+                vphase(std::integral_constant<int, 1>{});
+            else if (mode == 2)
+                vphase(std::integral_constant<int, 2>{});
+            else
+                vphase(std::integral_constant<int, 0>{});
         }
         // ---- flush (forward) ----------------------------------------------
         if (FWD && tile_ok) {
