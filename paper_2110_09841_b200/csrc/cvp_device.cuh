@@ -452,16 +452,18 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
 // -h exactly (clamp_mean, cvp.cpp:161-175, saturates), and only the NB
 // interior boundaries need evaluating. A voxel that occupies fewer rows gets
 // exactly -h at the interior boundaries below it, i.e. zero-share rows.
-// Rows m_first .. m_first + NB are emitted in order with max(share, 0) * inv_r2.
+// Rows m_first .. m_first + NB are emitted in order with
+// max(share, 0) * inv_r2 * wscale (the caller's mu * area, folded in here).
 template <int NB, class Emit>
 __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh, float pmh, float dz,
                                                float h, float sh, const bool per_row_r,
-                                               float inv_r2_fixed, Emit&& emit) {
+                                               float inv_r2_fixed, float wscale, Emit&& emit) {
     static_assert(NB == 1 || NB == 2, "one or two interior boundaries");
     constexpr float kMagic = 12582912.f;
     constexpr int kMagicBits = 0x4B400000;
     const float tr = fmaf(fabsf(dz), c.tr_b, c.tr_a);
-    const float clo = __fadd_ru(fmaxf(uh - tr, -2097152.f), kMagic - 1.f);
+    // (no +-2^21 guard: the brick's rows lie inside the detector)
+    const float clo = __fadd_ru(uh - tr, kMagic - 1.f);
     const int m_first = Mi + (__float_as_int(clo) - kMagicBits);
     // first interior boundary (top boundary of row m_first + 1), exact
     const float e1 = clo - (kMagic - 1.f);
@@ -469,17 +471,19 @@ __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh
         const float a1 = c.g * (uh - e1);
         const float p1 = clampf(a1, -h, h);
         const float t1 = clamp_mean_local(a1, sh * fabsf(pmh - e1), h);
-        float i0 = inv_r2_fixed, i1 = inv_r2_fixed;
+        // weight of a record = max(share, 0) * inv_r2 * wscale
+        float2 I = make_float2(inv_r2_fixed * wscale, inv_r2_fixed * wscale);
         if (per_row_r) {
             // midpoints of the plain row segments [p1, h] and [-h, p1] (cvp.cpp:223-229)
             const float2 Z = fma2(make_float2(p1, p1), make_float2(0.5f, 0.5f),
                                   make_float2(dz + 0.5f * h, dz - 0.5f * h));
             const float2 Q = fma2(Z, Z, make_float2(c.rho2, c.rho2));
-            i0 = fast_rcp(Q.x);
-            i1 = fast_rcp(Q.y);
+            I = mul2(make_float2(fast_rcp(Q.x), fast_rcp(Q.y)), make_float2(wscale, wscale));
         }
-        emit(m_first, fmaxf(h - t1, 0.f) * i0);
-        emit(m_first + 1, fmaxf(t1 + h, 0.f) * i1);
+        const float2 S = add2(make_float2(h, h), make_float2(-t1, t1));
+        const float2 W = mul2(make_float2(fmaxf(S.x, 0.f), fmaxf(S.y, 0.f)), I);
+        emit(m_first, W.x);
+        emit(m_first + 1, W.y);
     } else {
         const float2 E = make_float2(e1, e1 + 1.f);
         const float2 A = mul2(make_float2(c.g, c.g), sub2(make_float2(uh, uh), E));
@@ -492,19 +496,20 @@ __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh
         const float2 num = sub2(mul2(d1, d1), mul2(d2, d2));
         const float2 rr = make_float2(fast_rcp(fmaxf(s1, 1e-30f)), fast_rcp(fmaxf(s2, 1e-30f)));
         const float2 T = fma2(mul2(num, rr), make_float2(0.25f, 0.25f), make_float2(p1, p2));
-        const float2 W = sub2(make_float2(h, T.x), T);
-        float i0 = inv_r2_fixed, i1 = inv_r2_fixed, i2 = inv_r2_fixed;
+        const float2 S = sub2(make_float2(h, T.x), T);
+        float2 I = make_float2(inv_r2_fixed * wscale, inv_r2_fixed * wscale);
+        float i2 = I.x;
         if (per_row_r) {
             const float2 Z = fma2(add2(make_float2(h, p1), make_float2(p1, p2)), make_float2(0.5f, 0.5f),
                                   make_float2(dz, dz));
             const float z2 = fmaf(0.5f, p2 - h, dz);
             const float2 Q = fma2(Z, Z, make_float2(c.rho2, c.rho2));
-            i0 = fast_rcp(Q.x);
-            i1 = fast_rcp(Q.y);
-            i2 = fast_rcp(fmaf(z2, z2, c.rho2));
+            I = mul2(make_float2(fast_rcp(Q.x), fast_rcp(Q.y)), make_float2(wscale, wscale));
+            i2 = fast_rcp(fmaf(z2, z2, c.rho2)) * wscale;
         }
-        emit(m_first, fmaxf(W.x, 0.f) * i0);
-        emit(m_first + 1, fmaxf(W.y, 0.f) * i1);
+        const float2 W = mul2(make_float2(fmaxf(S.x, 0.f), fmaxf(S.y, 0.f)), I);
+        emit(m_first, W.x);
+        emit(m_first + 1, W.y);
         emit(m_first + 2, fmaxf(T.y + h, 0.f) * i2);
     }
 }

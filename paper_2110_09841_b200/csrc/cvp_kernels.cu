@@ -214,53 +214,66 @@ __device__ __forceinline__ CutRec load_cut(uint32_t sbase, int slot) {
 // Detector rectangle that contains every record a voxel of the brick can
 // emit under view vc: chi1 over the brick's base corners; chi2 over its z
 // range and its depth range widened by half a voxel-base diagonal (bound on
-// the elevation rectangle's depth spread |hw|*halfw). One extra pixel of
-// margin absorbs rounding; anything outside still lands correctly through the
-// global fallback path.
+// the elevation rectangle's depth spread |hw|*halfw). One extra column and
+// two extra rows of margin absorb rounding (the evaluation is float32: the
+// rectangle only needs pixel accuracy, and the same function sizes the tile
+// in tile_need_kernel); anything outside still lands correctly through the
+// global fallback path. The returned depths are the brick base's corner
+// depth range (unwidened).
 __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene& sc, int i0, int i1,
                                                 int j0, int j1, int k0, int k1, int& m0, int& m1,
-                                                int& n0, int& n1, double* depth_min = nullptr,
-                                                double* depth_max = nullptr,
+                                                int& n0, int& n1, float* depth_min = nullptr,
+                                                float* depth_max = nullptr,
                                                 bool* rows_inside = nullptr) {
-    const double xs[2] = {sc.minx + i0 * sc.a1, sc.minx + i1 * sc.a1};
-    const double ys[2] = {sc.miny + j0 * sc.a2, sc.miny + j1 * sc.a2};
-    double cmin = INFINITY, cmax = -INFINITY, dmin = INFINITY, dmax = -INFINITY;
+    // corner offsets from the source in float32 (|offset| <~ 1e3 mm: ~6e-5 mm)
+    const float xs[2] = {float(sc.minx + i0 * sc.a1 - vc.sx), float(sc.minx + i1 * sc.a1 - vc.sx)};
+    const float ys[2] = {float(sc.miny + j0 * sc.a2 - vc.sy), float(sc.miny + j1 * sc.a2 - vc.sy)};
+    const float w1x = float(vc.w1x), w1y = float(vc.w1y), w3x = float(vc.w3x), w3y = float(vc.w3y);
+    float cmin = INFINITY, cmax = -INFINITY, dmin = INFINITY, dmax = -INFINITY;
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) {
-            const double px = xs[a] - vc.sx, py = ys[b] - vc.sy;
-            const double d = vc.w3x * px + vc.w3y * py;
-            const double c1 = (vc.w1x * px + vc.w1y * py) / d;
-            cmin = fmin(cmin, c1);
-            cmax = fmax(cmax, c1);
-            dmin = fmin(dmin, d);
-            dmax = fmax(dmax, d);
+            const float d = w3x * xs[a] + w3y * ys[b];
+            const float c1 = (w1x * xs[a] + w1y * ys[b]) / d;
+            cmin = fminf(cmin, c1);
+            cmax = fmaxf(cmax, c1);
+            dmin = fminf(dmin, d);
+            dmax = fmaxf(dmax, d);
         }
     if (depth_min) *depth_min = dmin;
     if (depth_max) *depth_max = dmax;
-    const double margin = 0.5 * sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2);
-    dmin -= margin;
-    dmax += margin;
-    if (!(dmin > 0.0)) {
+    if (rows_inside) *rows_inside = false;
+    const float margin = float(0.5 * sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2));
+    const float dlo = dmin - margin, dhi = dmax + margin;
+    if (!(dlo > 0.f) || !(cmin > -1e7f) || !(cmax < 1e7f)) {
         m0 = 1;
         m1 = 0;
         n0 = 1;
         n1 = 0;
         return;
     }
-    const double zs[2] = {sc.minz + k0 * sc.a3 - vc.s3, sc.minz + k1 * sc.a3 - vc.s3};
-    double rmin = INFINITY, rmax = -INFINITY;
-    for (int a = 0; a < 2; ++a)
-        for (int b = 0; b < 2; ++b) {
-            const double d = b ? dmax : dmin;
-            const double c2 = vc.pp2 - zs[a] * vc.f_over_b2 / d;
-            rmin = fmin(rmin, c2);
-            rmax = fmax(rmax, c2);
+    const float fb2 = float(vc.f_over_b2), pp2 = float(vc.pp2);
+    const float z0 = float(sc.minz + k0 * sc.a3 - vc.s3), z1 = float(sc.minz + k1 * sc.a3 - vc.s3);
+    const float rlo = 1.f / dlo, rhi = 1.f / dhi;
+    // chi2 = pp2 - z fb2 / d is monotone in z and in 1/d: extremes at the corners
+    float rmin = INFINITY, rmax = -INFINITY;
+    for (float z : {z0, z1})
+        for (float r : {rlo, rhi}) {
+            const float c2 = pp2 - z * fb2 * r;
+            rmin = fminf(rmin, c2);
+            rmax = fmaxf(rmax, c2);
         }
-    n0 = max(int(ceil(cmin - 0.5)) - 1, 0);
-    n1 = min(int(floor(cmax + 0.5)) + 1, sc.cols - 1);
+    if (!(rmin > -1e7f) || !(rmax < 1e7f)) {
+        m0 = 1;
+        m1 = 0;
+        n0 = 1;
+        n1 = 0;
+        return;
+    }
+    n0 = max(int(ceilf(cmin - 0.5f)) - 1, 0);
+    n1 = min(int(floorf(cmax + 0.5f)) + 1, sc.cols - 1);
     // two rows of margin: the fast row walk (walk_rows_fast) emits up to one
     // row past a voxel's range, whose own bound carries float slack
-    const int r0 = int(ceil(rmin - 0.5)) - 2, r1 = int(floor(rmax + 0.5)) + 2;
+    const int r0 = int(ceilf(rmin - 0.5f)) - 2, r1 = int(floorf(rmax + 0.5f)) + 2;
     m0 = max(r0, 0);
     m1 = min(r1, sc.rows - 1);
     if (rows_inside) *rows_inside = r0 >= 0 && r1 <= sc.rows - 1;
@@ -366,25 +379,45 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
         auto footprint = [&]() {
             int m0, m1, n0, n1;
             bool fixed_ok = true, rows_inside = false;
-            double dmin = 0.0, dmax = 0.0;
+            float dmin = 0.f, dmax = 0.f;
             brick_footprint(vc, sc, i0, i1, j0, j1, k0, k1, m0, m1, n0, n1, &dmin, &dmax, &rows_inside);
+            const float diag = float(sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2));
+            const float fb2 = float(vc.f_over_b2);
             // Row-walk mode of this (brick, view): the fast walk needs every
             // voxel's rows inside the detector (no clamping), a full brick
             // along x3 (no virtual layers) and 2 tr < NB + 1 for every
             // voxel-cut, with the rigorous bound
             //   tr <= h f/(b2 (dmin - dd)) + |dz|max f dd / (b2 dmin (dmin - dd)) + 1e-5,
-            // dd = diag/2 >= |hw| halfw (walk_rows_fast, cvp_device.cuh).
+            // dd = diag/2 >= |hw| halfw (walk_rows_fast, cvp_device.cuh);
+            // and (elevation correction) the gate dz^2 > 1e-28 rho^2
+            // (cvp.cpp:353-355) true for every voxel-cut: |dz| at the layer
+            // nearest the source plane against rho <= the largest source
+            // distance of the brick's base corners.
             {
                 int mode = 0;
-                const double ddm = 0.5 * sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2);
-                const double dl = dmin - ddm;
-                if (rows_inside && k1 == k0 + BK && dl > 0.0) {
-                    const double zlo = sc.minz + (k0 + 0.5) * sc.a3 - vc.s3;
-                    const double zhi = sc.minz + (k1 - 0.5) * sc.a3 - vc.s3;
-                    const double dzm = fmax(fabs(zlo), fabs(zhi));
-                    const double tr = 0.5 * sc.a3 * vc.f_over_b2 / dl +
-                                      dzm * vc.f_over_b2 * ddm / (dmin * dl) + 2e-5;
-                    mode = 2.0 * tr < 0.999 ? 1 : 2.0 * tr < 1.999 ? 2 : 0;
+                const float ddm = 0.5f * diag;
+                const float dl = dmin - ddm;
+                const float zlo = float(sc.minz + (k0 + 0.5) * sc.a3 - vc.s3);
+                const float zhi = float(sc.minz + (k1 - 0.5) * sc.a3 - vc.s3);
+                float dz_near;
+                if (zlo > 0.f || zhi < 0.f) {
+                    dz_near = fminf(fabsf(zlo), fabsf(zhi));
+                } else {
+                    const double t = rint(-(sc.minz + (k0 + 0.5) * sc.a3 - vc.s3) / sc.a3);
+                    dz_near = float(fabs(sc.minz + (k0 + 0.5 + t) * sc.a3 - vc.s3));
+                }
+                float rho2max = 0.f;
+                for (int q = 0; q < 4; ++q) {
+                    const float x = float(sc.minx + ((q & 1) ? i1 : i0) * sc.a1 - vc.sx);
+                    const float y = float(sc.miny + ((q & 2) ? j1 : j0) * sc.a2 - vc.sy);
+                    rho2max = fmaxf(rho2max, x * x + y * y);
+                }
+                const bool gate_ok = !corr || dz_near * dz_near > 4e-28f * rho2max;
+                if (rows_inside && k1 == k0 + BK && dl > 0.f && gate_ok) {
+                    const float dzm = fmaxf(fabsf(zlo), fabsf(zhi));
+                    const float rdl = 1.f / dl;
+                    const float tr = (0.5f * float(sc.a3) + dzm * ddm / dmin) * fb2 * rdl * 1.0001f + 2e-5f;
+                    mode = 2.f * tr < 0.999f ? 1 : 2.f * tr < 1.999f ? 2 : 0;
                 }
                 s.walk_mode = mode;
             }
@@ -397,19 +430,21 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 //     column's wedge between depths dmin..dmax <= b1 dmax/f (dmax-dmin);
                 //   sum over a column stack of one row's shares <= the row's
                 //     z-window at the widest elevation depth <= b2 (dmax + diag/2)/f.
-                // Scale 2^30 / bound keeps every partial inside int32.
-                const double diag = sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2);
-                const double area = vc.b1 * dmax / vc.f * fmax(dmax - dmin, 1e-30 * dmax);
-                const double zwin = vc.b2 * (dmax + 0.5 * diag) / vc.f;
-                const double bound = double(s.mu_abs_max) * area * zwin / (dmin * dmin) * 1.05;
-                const double q = (bound > 0.0 && dmin > 0.0) ? 1073741824.0 / bound : 0.0;
+                // Scale 2^30 / bound keeps every partial inside int32 (float32
+                // evaluation with 5% slack).
+                const float bf = float(vc.b2_over_f);
+                const float b1f = float(vc.b1 / vc.f);
+                const float area = b1f * dmax * fmaxf(dmax - dmin, 1e-30f * dmax);
+                const float zwin = bf * (dmax + 0.5f * diag);
+                const float bound = s.mu_abs_max * (area * zwin / (dmin * dmin)) * 1.05f;
+                const float q = (bound > 0.f && dmin > 0.f) ? 1073741824.f / bound : 0.f;
                 // the fixed-point tile needs a finite brick and a normal
                 // float32 scale; otherwise (NaN / Inf voxels, |mu| so small
                 // that 2^30 / bound overflows) every record of this (brick,
                 // view) takes the float-atomic path below, which propagates
                 // NaN / Inf like the reference's double accumulation
-                fixed_ok = !s.nonfinite && q > 0.0 && q < 3.0e38 && float(q) >= 1.17549435e-38f;
-                s.qscale = fixed_ok ? float(q) : 0.f;
+                fixed_ok = !s.nonfinite && q > 0.f && q < 3.0e38f && q >= 1.17549435e-38f;
+                s.qscale = fixed_ok ? q : 0.f;
             }
             const int tr = max(m1 - m0 + 1, 0), tc = max(n1 - n0 + 1, 0);
             const int stride = tr | 1;
@@ -431,6 +466,33 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             const double zc64 = sc.minz + (k0 + kk + 0.5) * sc.a3;
             s.dz[kk] = EXACT ? float(zc64 - vc.s3) : float(zc64) - float(vc.s3);
         }
+        // forward (no tile staging): the column loads are split over two
+        // threads per column (slots 0-1 and 2-3), halving the dependent
+        // L2-latency chain of the G-phase
+        constexpr bool SPLIT_LOAD = FWD && 2 * NCOL <= NT;
+        // (thread NCOL computes the footprint instead: column 0 keeps all slots)
+        if (SPLIT_LOAD && tid > NCOL && tid < 2 * NCOL) {
+            const int c = tid - NCOL;
+            const int i = i0 + (c % BI), j = j0 + (c / BI);
+            if (i < i1 && j < j1 && s.nonzero[c]) {
+                // slots 2-3 unconditionally (no wait for the count: one L2
+                // round trip; unused slots are never read)
+                const size_t col = size_t(j) * sc.n1 + i;
+                const size_t vl = size_t(v - p.t.v0);
+                float4 ra[MAXC - 2], rb[MAXC - 2];
+#pragma unroll
+                for (int q = 2; q < MAXC; ++q) {
+                    const size_t slot = (vl * MAXC + q) * p.t.ncols + col;
+                    ra[q - 2] = __ldg(p.t.cutA + slot);
+                    rb[q - 2] = __ldg(p.t.cutB + slot);
+                }
+#pragma unroll
+                for (int q = 2; q < MAXC; ++q) {
+                    s.cutA[q * NCOL + c] = ra[q - 2];
+                    s.cutB[q * NCOL + c] = rb[q - 2];
+                }
+            }
+        }
         if (tid < NCOL) {
             const int c = tid;
             const int i = i0 + (c % BI), j = j0 + (c / BI);
@@ -443,11 +505,33 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 const size_t vl = size_t(v - p.t.v0);
                 const size_t base = vl * p.t.ncols + col;
                 cnt = __ldg(p.t.count + base);
-                const int nc = min(cnt, MAXC);
-                for (int q = 0; q < nc; ++q) {
-                    const size_t slot = (vl * MAXC + q) * p.t.ncols + col;
-                    s.cutA[q * NCOL + c] = __ldg(p.t.cutA + slot);
-                    s.cutB[q * NCOL + c] = __ldg(p.t.cutB + slot);
+                if (SPLIT_LOAD) {
+                    // slots 0-1 issued with the count (one L2 round trip)
+                    float4 ra[2], rb[2];
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const size_t slot = (vl * MAXC + q) * p.t.ncols + col;
+                        ra[q] = __ldg(p.t.cutA + slot);
+                        rb[q] = __ldg(p.t.cutB + slot);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        s.cutA[q * NCOL + c] = ra[q];
+                        s.cutB[q * NCOL + c] = rb[q];
+                    }
+                    if (c == 0)  // (thread NCOL computes the footprint)
+                        for (int q = 2; q < min(cnt, MAXC); ++q) {
+                            const size_t slot = (vl * MAXC + q) * p.t.ncols + col;
+                            s.cutA[q * NCOL + c] = __ldg(p.t.cutA + slot);
+                            s.cutB[q * NCOL + c] = __ldg(p.t.cutB + slot);
+                        }
+                } else {
+                    const int nc = min(cnt, MAXC);
+                    for (int q = 0; q < nc; ++q) {
+                        const size_t slot = (vl * MAXC + q) * p.t.ncols + col;
+                        s.cutA[q * NCOL + c] = __ldg(p.t.cutA + slot);
+                        s.cutB[q * NCOL + c] = __ldg(p.t.cutB + slot);
+                    }
                 }
                 const ColumnAnchor an = column_anchor<EXACT>(
                     vc.pp2, sc.minz + (k0 + 0.5) * sc.a3 - vc.s3, __ldg(p.t.Q0 + base), sc.a3);
@@ -573,25 +657,24 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             // fast walk (MODE 1 / 2): rows need no clamping and stay inside
             // the tile (2-row margin), so the addresses need no bound
             auto fast_cut = [&](const CutRec& r, VoxState& v) {
-                const float sh = (corr && r.rho2 < v.dz2e28) ? r.shw : 0.f;
+                // (fast mode: the elevation gate holds for every voxel-cut of
+                // the brick, footprint())
+                const float sh = corr ? r.shw : 0.f;
                 const float uh = fmaf(v.dz, r.kc, v.u0h);
                 const uint32_t cbase = tbase + 4u * uint32_t((r.n - tn0) * tstride - tm0);
-                const float wA = FWD ? v.muq * r.A : r.A;
-                float cut_acc = 0.f;
                 int nrow = 0;
-                auto emit = [&](int m, float wr) {
+                auto emit = [&](int m, float w) {
                     uint32_t a = cbase + 4u * uint32_t(m);
                     if (MODE == 2 && nrow == 2) a = tbase + 4u * min(uint32_t((r.n - tn0) * tstride + m - tm0),
                                                                     uint32_t((r.n - tn0) * tstride) + trm1);
                     ++nrow;
                     if (FWD)
-                        red_s32(a, __float2int_rn(wr * wA));
+                        red_s32(a, __float2int_rn(w));
                     else
-                        cut_acc = fmaf(lds_f32(a), wr, cut_acc);
+                        v.acc = fmaf(lds_f32(a), w, v.acc);
                 };
                 walk_rows_fast<MODE == 2 ? 2 : 1>(r, v.Mi, uh, v.pmh, v.dz, h, sh, per_row_r,
-                                                  v.inv_r2_fixed, emit);
-                if (!FWD) v.acc = fmaf(wA, cut_acc, v.acc);
+                                                  v.inv_r2_fixed, FWD ? v.muq * r.A : r.A, emit);
             };
             auto cut = [&](const CutRec& r) {
                 if (tile_ok && unsigned(r.n - tn0) < unsigned(tcols)) {
@@ -641,17 +724,26 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 vphase(std::integral_constant<int, 0>{});
         }
         // ---- flush (forward) ----------------------------------------------
+        // Lanes cover a power-of-two span of tile columns (coalesced float
+        // atomics along an image row), warps and lane groups stride the rows:
+        // no integer division in the loop.
         if (FWD && tile_ok) {
             __syncthreads();
-            const int ntile = trows * tcols;
             const float inv_qs = qs > 0.f ? 1.f / qs : 0.f;
-            for (int idx = tid; idx < ntile; idx += NT) {
-                const int r = idx / tcols, cc = idx % tcols;
-                const int q = itile[cc * tstride + r];
-                if (q != 0) {
-                    itile[cc * tstride + r] = 0;
-                    const size_t px = size_t(tm0 + r) * cols + (tn0 + cc);
-                    atomicAdd(s.img + px, float(q) * inv_qs);
+            const int span = tcols >= 32 ? 32 : tcols > 16 ? 32 : tcols > 8 ? 16 : tcols > 4 ? 8 : 4;
+            const int lsh = 31 - __clz(span);             // log2(span)
+            const int sub = lane >> lsh, rstep = NWARP << (5 - lsh);
+            float* img = s.img + size_t(tm0) * cols + tn0;
+            for (int c0 = 0; c0 < tcols; c0 += span) {
+                const int cc = c0 + (lane & (span - 1));
+                if (cc >= tcols) continue;
+                int* col = itile + cc * tstride;
+                for (int r = (warp << (5 - lsh)) + sub; r < trows; r += rstep) {
+                    const int q = col[r];
+                    if (q != 0) {
+                        col[r] = 0;
+                        atomicAdd(img + size_t(r) * cols + cc, float(q) * inv_qs);
+                    }
                 }
             }
         }
