@@ -56,6 +56,13 @@ int orc_backproject_siddon(const int* counts, const double* voxel, int rows, int
                            double ph, int n_views, const double* views17, int k_per_edge,
                            const double* proj, double* out);
 
+/* SF-TT separable-footprint pair (tt_oracle.c; Long, Fessler & Balter 2010),
+ * amplitude 0 = A1 (voxel-centre elevation), 1 = A2 (per detector row). */
+int orc_project_tt(const int* counts, const double* voxel, int rows, int cols, int n_views,
+                   const double* views17, int amplitude, const double* vol, double* out);
+int orc_backproject_tt(const int* counts, const double* voxel, int rows, int cols, int n_views,
+                       const double* views17, int amplitude, const double* proj, double* out);
+
 /* Kahan-compensated dot (solver.cpp:15-24). */
 double orc_dot_kahan(const double* a, const double* b, size_t n);
 

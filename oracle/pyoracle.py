@@ -215,6 +215,27 @@ class Restatement(_Checker):
     def __init__(self, path=RESTATEMENT_SO):
         super().__init__(path)
 
+    # SF-TT (oracle/tt_oracle.c): Long, Fessler & Balter 2010, float64
+    def project_tt(self, sc: Scene, vol, amplitude=1):
+        counts, voxel, views = self._geom(sc)
+        vol = np.ascontiguousarray(vol, dtype=np.float64).ravel()
+        out = np.zeros(sc.npx())
+        f = self._fn("project_tt")
+        f.argtypes = [_ip, _dp, C.c_int, C.c_int, C.c_int, _dp, C.c_int, _dp, _dp]
+        self._check(f(_i(counts), _d(voxel), sc.rows, sc.cols, sc.n_views, _d(views),
+                      int(amplitude), _d(vol), _d(out)))
+        return out.reshape(sc.n_views, sc.rows, sc.cols)
+
+    def backproject_tt(self, sc: Scene, proj, amplitude=1):
+        counts, voxel, views = self._geom(sc)
+        proj = np.ascontiguousarray(proj, dtype=np.float64).ravel()
+        out = np.zeros(sc.nvox())
+        f = self._fn("backproject_tt")
+        f.argtypes = [_ip, _dp, C.c_int, C.c_int, C.c_int, _dp, C.c_int, _dp, _dp]
+        self._check(f(_i(counts), _d(voxel), sc.rows, sc.cols, sc.n_views, _d(views),
+                      int(amplitude), _d(proj), _d(out)))
+        return out.reshape(sc.counts[2], sc.counts[1], sc.counts[0])
+
 
 class Reference(_Checker):
     prefix = "ref_"

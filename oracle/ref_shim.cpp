@@ -10,6 +10,7 @@
 // principal point [2], pixel size [2]; they are rebuilt with the reference's
 // own ViewGeometry::make (geometry.cpp:52-88) so both sides of a parity test
 // see bit-identical view parameters.
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <cstring>
@@ -20,6 +21,7 @@
 #include <vector>
 
 #include "cbct/cvp.hpp"
+#include "cbct/den.hpp"
 #include "cbct/geometry.hpp"
 #include "cbct/siddon.hpp"
 #include "cbct/solver.hpp"
@@ -309,6 +311,39 @@ int ref_cgls(const int* counts, const double* voxel, int rows, int cols, double 
         std::memcpy(x_out, r.x.values.data(), sizeof(double) * r.x.values.size());
         std::memcpy(residuals_out, r.residual_norms.data(),
                     sizeof(double) * r.residual_norms.size());
+    });
+}
+
+// DEN I/O (den.cpp:27-100): write (y, x, z, float32 payload) / read back.
+int ref_den_write(const char* path, int y, int x, int z, const float* values) {
+    return guarded([&] {
+        DenFile d;
+        d.dim_y = std::uint16_t(y);
+        d.dim_x = std::uint16_t(x);
+        d.dim_z = std::uint16_t(z);
+        d.values.assign(values, values + d.value_count());
+        den_write(path, d);
+    });
+}
+
+// dims_out[3] = (y, x, z); copies at most cap values
+int ref_den_read(const char* path, int* dims_out, float* values, std::size_t cap) {
+    return guarded([&] {
+        DenFile d = den_read(path);
+        dims_out[0] = d.dim_y;
+        dims_out[1] = d.dim_x;
+        dims_out[2] = d.dim_z;
+        std::memcpy(values, d.values.data(), sizeof(float) * std::min(cap, d.values.size()));
+    });
+}
+
+// volume -> DEN -> file (to_den of an AttenuationVolume, float64 -> float32)
+int ref_den_write_volume(const char* path, const int* counts, const double* voxel,
+                         const double* values) {
+    return guarded([&] {
+        auto g = VolumeGeometry::make({counts[0], counts[1], counts[2]}, {voxel[0], voxel[1], voxel[2]});
+        AttenuationVolume v{g, std::vector<double>(values, values + g.voxel_count())};
+        den_write(path, to_den(v));
     });
 }
 

@@ -80,3 +80,76 @@ def test_device_loader_matches_layout(tmp_path):
     assert torch.equal(t.cpu().view(-1), torch.arange(24, dtype=torch.float32))
     den.den_write_device(tmp_path / "w.den", t)
     assert open(tmp_path / "v.den", "rb").read() == open(tmp_path / "w.den", "rb").read()
+
+
+# ---- byte-exact parity with the reference's own den.cpp (oracle/_ref) -------
+
+def _ref_lib():
+    import ctypes as C
+    from oracle import pyoracle
+    if not pyoracle.reference_available():
+        pytest.skip("oracle/_ref not built")
+    lib = C.CDLL(pyoracle.REFERENCE_SO)
+    lib.ref_den_write.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]
+    lib.ref_den_read.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_float), C.c_size_t]
+    lib.ref_den_write_volume.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double)]
+    lib.ref_last_error.restype = C.c_char_p
+    return lib
+
+
+def test_den_bytes_match_the_reference_writer(tmp_path):
+    """den.py and the reference's den_write produce identical files; each
+    reads the other's file back to the same values (den.cpp:27-68)."""
+    import ctypes as C
+    lib = _ref_lib()
+    rng = np.random.default_rng(5)
+    vals = (rng.standard_normal(7 * 5 * 3) * 1e3).astype(np.float32)
+    vals[:4] = [0.0, -0.0, np.inf, np.nan]
+    ours, theirs = tmp_path / "ours.den", tmp_path / "theirs.den"
+    den.den_write(ours, den.DenFile(7, 5, 3, vals))
+    assert lib.ref_den_write(str(theirs).encode(), 7, 5, 3,
+                             vals.ctypes.data_as(C.POINTER(C.c_float))) == 0
+    assert open(ours, "rb").read() == open(theirs, "rb").read()
+    dims = (C.c_int * 3)()
+    back = np.zeros(vals.size, dtype=np.float32)
+    assert lib.ref_den_read(str(ours).encode(), dims, back.ctypes.data_as(C.POINTER(C.c_float)),
+                            back.size) == 0
+    assert tuple(dims) == (7, 5, 3)
+    assert back.tobytes() == vals.tobytes()
+    d = den.den_read(theirs)
+    assert (d.dim_y, d.dim_x, d.dim_z) == (7, 5, 3) and d.values.tobytes() == vals.tobytes()
+
+
+def test_den_volume_mapping_matches_the_reference(tmp_path):
+    """to_den of a float64 volume (N2, N1, N3 header, float32 payload):
+    byte-identical to the reference's to_den + den_write (den.cpp:70-79)."""
+    import ctypes as C
+    lib = _ref_lib()
+    geom = cb.VolumeGeometry.make((6, 4, 3), (0.5, 0.25, 1.0))
+    x = cb.fill_uniform01(geom.voxel_count(), 11) * 3.0 - 1.0
+    ours, theirs = tmp_path / "v_ours.den", tmp_path / "v_theirs.den"
+    den.den_write(ours, den.to_den(cb.AttenuationVolume(geom, x)))
+    counts = (C.c_int * 3)(6, 4, 3)
+    voxel = (C.c_double * 3)(0.5, 0.25, 1.0)
+    assert lib.ref_den_write_volume(str(theirs).encode(), counts, voxel,
+                                    x.ctypes.data_as(C.POINTER(C.c_double))) == 0
+    assert open(ours, "rb").read() == open(theirs, "rb").read()
+
+
+def test_den_reference_rejects_what_den_py_rejects(tmp_path):
+    """Malformed files: both sides refuse (size mismatch, truncated header)."""
+    import ctypes as C
+    lib = _ref_lib()
+    bad = tmp_path / "bad.den"
+    bad.write_bytes(np.array([2, 2, 2], dtype="<u2").tobytes() + b"\0" * 8)
+    dims = (C.c_int * 3)()
+    buf = np.zeros(8, dtype=np.float32)
+    assert lib.ref_den_read(str(bad).encode(), dims, buf.ctypes.data_as(C.POINTER(C.c_float)), 8) != 0
+    with pytest.raises(cb.CvpbRuntimeError):
+        den.den_read(bad)
+    short = tmp_path / "short.den"
+    short.write_bytes(b"\1\0")
+    assert lib.ref_den_read(str(short).encode(), dims, buf.ctypes.data_as(C.POINTER(C.c_float)), 8) != 0
+    with pytest.raises(cb.CvpbRuntimeError):
+        den.den_read(short)
