@@ -493,6 +493,19 @@ def run_native(args):
                 "kernel": dom, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "note": "4 B/voxel-view (SURVEY 8d); the kernel is issue-bound, see DESIGN.md"}
+    # secondary roof: shared-memory int32 atomic updates of the
+    # forward's detector tile, U = 4.22 updates per voxel-view at c3 (the
+    # reference's collect_cut_records over 20,000 random voxel-views), against
+    # the microbenchmarked red.shared.add.s32 peak (tools/smem_atomic_peak.cu)
+    ap = _profile_file("smem_atomic_peak_r02.json")
+    if ap:
+        with open(ap) as f:
+            peak_ups = json.load(f)["results"][0]["updates_per_s"]
+        ups = work / world / (pm * 1e-3) * 1e9 * 4.22
+        roofline["smem_atomic"] = {"bound": "shared atomics", "achieved": ups, "peak": peak_ups,
+                                   "unit": "updates/s", "frac": ups / peak_ups,
+                                   "U_per_voxel_view": 4.22,
+                                   "source": os.path.relpath(ap, ROOT)}
     sp = (_profile_file("ncu_r02_fwd_summary.txt", "ncu_r01_fwd_summary.txt") if fwd_dom else
           _profile_file("ncu_r02_bwd_summary.txt", "ncu_r01_bwd_summary.txt"))
     if sp:

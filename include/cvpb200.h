@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define CVPB_ABI_VERSION 2
+#define CVPB_ABI_VERSION 3
 
 typedef enum cvpb_status {
     CVPB_OK = 0,
@@ -264,6 +264,63 @@ int cvpb_vec_sart_update(cvpb_context* ctx, float* x, const float* corr, const f
 int cvpb_cgls(cvpb_context* ctx, int projector, const cvpb_cvp_options* cvp_opts,
               const cvpb_tt_options* tt_opts, const cvpb_exec_policy* exec, int k_per_edge,
               const float* d_b, float* d_x, int iterations, double* residual_norms, void* stream);
+
+/* ---- multi-device scenes ------------------------------------
+ * One process drives several GPUs: a group holds one context per member
+ * device with the same scene. Views are sharded in contiguous ranges (member
+ * g owns views [V g / N, V (g+1) / N)); the volume is sharded in contiguous
+ * z-slabs (planes [N3 g / N, N3 (g+1) / N)), the k-slowest layout of
+ * geometry.hpp:34-36 making each slab one contiguous range.
+ *   forward   each member uploads its slab of the host volume, the slabs are
+ *             all-gathered over NVLink (peer copies), and each member
+ *             projects its views into its part of the host stack — no
+ *             exchange of projections at all;
+ *   backward  each member backprojects its views into a full partial volume,
+ *             then reduce-scatters the partials over peer memory (one kernel
+ *             per member reads its slab out of every member's partial, sums
+ *             the members in a fixed order in float64) and writes its slab of
+ *             the host volume.
+ * Members may repeat a device (e.g. {0, 0}): the same code then runs with
+ * every member on one GPU, which is how the multi-device path is tested on a
+ * single-GPU box. With one member every call is the single-context call.
+ * The reference entry points these replace for an unchanged C++ caller:
+ * project_cvp_into / backproject_cvp_into (cvp.hpp:87-99) — the drop-in
+ * (libcbct_b200) builds its scenes as groups over every visible GPU, or over
+ * the devices listed in CBCT_B200_DEVICES (e.g. "0,0"). */
+typedef struct cvpb_group cvpb_group;
+/* devices == NULL or n_devices == 0: every visible device. At most 16 members. */
+int cvpb_group_create(const int* devices, int n_devices, cvpb_group** out);
+void cvpb_group_destroy(cvpb_group* g);
+int cvpb_group_size(const cvpb_group* g, int* n_members);
+/* member m's device, view shard and volume slab (elements) — after set_geometry */
+int cvpb_group_member(const cvpb_group* g, int member, int* device, int* view_begin,
+                      int* view_count, size_t* slab_begin, size_t* slab_count);
+/* member m's context (single-device calls on the same scene, e.g. Siddon) */
+int cvpb_group_context(cvpb_group* g, int member, cvpb_context** out);
+int cvpb_group_set_geometry(cvpb_group* g, const cvpb_volume_geometry* vol,
+                            const cvpb_detector_geometry* det, int n_views, const cvpb_view* views);
+/* project_cvp_into / backproject_cvp_into over the group (float64 host
+ * buffers, reference semantics; view_seconds[v] = the owning member's time
+ * per view). */
+int cvpb_group_project_cvp_host(cvpb_group* g, const cvpb_cvp_options* opts,
+                                const cvpb_exec_policy* exec, const double* volume, double* proj,
+                                double* view_seconds);
+int cvpb_group_backproject_cvp_host(cvpb_group* g, const cvpb_cvp_options* opts,
+                                    const cvpb_exec_policy* exec, const double* proj,
+                                    double* volume, double* view_seconds);
+int cvpb_group_project_tt_host(cvpb_group* g, const cvpb_tt_options* opts, const double* volume,
+                               double* proj);
+int cvpb_group_backproject_tt_host(cvpb_group* g, const cvpb_tt_options* opts, const double* proj,
+                                   double* volume);
+/* cgls (solver.cpp:55-106) device-resident across the group: per iteration
+ * one sharded P (after an all-gather of the direction's slabs), one sharded
+ * BP + peer reduce-scatter into slabs, slab-local vector updates; the dots
+ * are summed over the members in a fixed order (float64). Same arguments and
+ * early exits as cvpb_cgls_host. */
+int cvpb_group_cgls_host(cvpb_group* g, int projector, const cvpb_cvp_options* cvp_opts,
+                         const cvpb_tt_options* tt_opts, const cvpb_exec_policy* exec,
+                         int k_per_edge, const double* b, double* x, int iterations,
+                         double* residual_norms);
 
 #ifdef __cplusplus
 }

@@ -11,7 +11,7 @@ from ._native import (CvpbRuntimeError, DomainError, InvalidArgument, NoDevice, 
 from .geometry import (AttenuationVolume, DetectorGeometry, ProjectionStack, ViewGeometry,
                        VolumeGeometry, make_circular_trajectory, read_camera_matrices,
                        views_to_array, write_camera_matrices)
-from .operators import (CutVolumeRecord, CvpOptions, CvpPrecision, DeviceScene, ExecPolicy,
+from .operators import (CutVolumeRecord, CvpOptions, CvpPrecision, DeviceScene, ExecPolicy, GroupScene,
                         PixelRoi, PixelScaling, RadiusEstimate, TTOptions, backproject_cvp,
                         backproject_cvp_into, backproject_siddon_k, backproject_siddon_k_into,
                         collect_cut_records, pixel_scale_cos, pixel_scale_exact, project_cvp,

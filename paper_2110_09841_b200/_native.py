@@ -108,6 +108,22 @@ SIGNATURES = {
     "cvpb_vec_sart_update": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, C.c_int, C.c_size_t, _vp]),
     "cvpb_cgls": (C.c_int, [_vp, C.c_int, _P(cvpb_cvp_options), _P(cvpb_tt_options),
                             _P(cvpb_exec_policy), C.c_int, _vp, _vp, C.c_int, _dp, _vp]),
+    # multi-device scenes
+    "cvpb_group_create": (C.c_int, [_ip, C.c_int, _P(_vp)]),
+    "cvpb_group_destroy": (None, [_vp]),
+    "cvpb_group_size": (C.c_int, [_vp, _ip]),
+    "cvpb_group_member": (C.c_int, [_vp, C.c_int, _ip, _ip, _ip, _P(C.c_size_t), _P(C.c_size_t)]),
+    "cvpb_group_context": (C.c_int, [_vp, C.c_int, _P(_vp)]),
+    "cvpb_group_set_geometry": (C.c_int, [_vp, _P(cvpb_volume_geometry),
+                                          _P(cvpb_detector_geometry), C.c_int, _P(cvpb_view)]),
+    "cvpb_group_project_cvp_host": (C.c_int, [_vp, _P(cvpb_cvp_options), _P(cvpb_exec_policy),
+                                              _vp, _vp, _vp]),
+    "cvpb_group_backproject_cvp_host": (C.c_int, [_vp, _P(cvpb_cvp_options),
+                                                  _P(cvpb_exec_policy), _vp, _vp, _vp]),
+    "cvpb_group_project_tt_host": (C.c_int, [_vp, _P(cvpb_tt_options), _vp, _vp]),
+    "cvpb_group_backproject_tt_host": (C.c_int, [_vp, _P(cvpb_tt_options), _vp, _vp]),
+    "cvpb_group_cgls_host": (C.c_int, [_vp, C.c_int, _P(cvpb_cvp_options), _P(cvpb_tt_options),
+                                       _P(cvpb_exec_policy), C.c_int, _vp, _vp, C.c_int, _dp]),
 }
 
 # status code -> exception type the reference throws for the same condition

@@ -232,6 +232,9 @@ struct cvpb_context {
     DevBuf<float> cg_r, cg_q, cg_s, cg_p;
     DevBuf<double> cg_partials, cg_hist;
     DevBuf<cvpb::CgState> cg_state;
+    DevBuf<unsigned long long> d_det;  // deterministic forward: int64 merge stack
+    DevBuf<double> d_det_g;
+    DevBuf<unsigned int> d_det_max;
     DevBuf<int> d_rec_i;
     DevBuf<double> d_rec_d;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -395,6 +398,19 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     L.vol_copy = vol_in64 ? const_cast<float*>(vol_in) : nullptr;
     L.vol_out64 = vol_out64;
     L.err = ctx->d_err.p;
+    if (forward && L.deterministic && view_count > 0) {
+        // bricks merge in int64 fixed point (order-independent): P is
+        // bit-reproducible like the reference's deterministic ExecPolicy
+        // (exec.hpp:6-15); 8 B per pixel of the launch
+        CVPB_CUDA(ctx->d_det.reserve(ctx->npx_view() * size_t(view_count)));
+        CVPB_CUDA(ctx->d_det_g.reserve(1));
+        CVPB_CUDA(ctx->d_det_max.reserve(1));
+        L.det_acc = ctx->d_det.p;
+        L.det_g = ctx->d_det_g.p;
+        L.det_maxbits = ctx->d_det_max.p;
+        const double vv = ctx->vol.voxel_size[0] * ctx->vol.voxel_size[1] * ctx->vol.voxel_size[2];
+        L.det_factor = double(ctx->nvox()) * vv / std::max(ctx->r_min * ctx->r_min, 1e-300);
+    }
     if (!forward && view_count == 0 && !accumulate) {
         CVPB_CUDA(cudaMemsetAsync(vol_out, 0, sizeof(float) * ctx->nvox(), st));
         return CVPB_OK;
@@ -591,6 +607,10 @@ int host_roundtrip(cvpb_context* ctx, bool vol_to_proj, const double* in, double
 }
 }  // namespace
 
+namespace cvpb {
+int set_last_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace cvpb
+
 extern "C" {
 
 int cvpb_abi_version(void) { return CVPB_ABI_VERSION; }
@@ -643,6 +663,9 @@ void cvpb_context_destroy(cvpb_context* ctx) {
     ctx->d_stage.release();
     ctx->d_cut_table.release();
     ctx->d_rec_i.release();
+    ctx->d_det.release();
+    ctx->d_det_g.release();
+    ctx->d_det_max.release();
     ctx->d_rec_d.release();
     ctx->cg_partials.release();
     ctx->h_in64.release();

@@ -125,6 +125,12 @@ struct CvpParams {
     int tile_cap;
     int accumulate;           // backward: add into vol_out
     int atomic_out;           // backward: several view groups -> atomicAdd
+    // forward, ExecPolicy::deterministic: bricks merge into an int64
+    // fixed-point stack (view_begin-relative) at the launch-wide scale *det_g
+    // (integer adds commute: the result is bit-reproducible); *det_g == 0
+    // (non-finite volume) falls back to the float atomics
+    unsigned long long* det_acc;
+    const double* det_g;
     int* err;
 };
 
@@ -140,6 +146,8 @@ struct Smem {
     int nonzero[NCOL];        // forward: the column holds a nonzero attenuation
     float vox[NCOL * MUS];    // forward: mu; backward: accumulators
     float* img;               // this view's image (forward: output, backward: input)
+    unsigned long long* dimg; // forward, deterministic: this view's int64 image (else null)
+    double det_g;             // forward, deterministic: fixed-point scale (0: float atomics)
     const float* scale;       // backward: this view's phase-2 factors
     int tile_m0, tile_n0, tile_rows, tile_cols, tile_stride, tile_ok;
     float mu_abs_max;         // forward: max |mu| over the brick
@@ -317,6 +325,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
     if (tid == 0) {
         s.mu_abs_max = 0.f;
         s.nonfinite = 0;
+        s.det_g = (FWD && p.det_g) ? *p.det_g : 0.0;
     }
     // forward: the fixed-point tile starts zeroed and every flush re-zeroes
     // the pixels it reads, so views need no zeroing pass of their own
@@ -457,6 +466,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             s.tile_ok = (tr > 0 && tc > 0 && stride * tc <= p.tile_cap && (!FWD || fixed_ok)) ? 1 : 0;
             const size_t vl = size_t(v - p.view_begin);
             s.img = FWD ? p.proj_out + vl * npx : const_cast<float*>(p.proj_in) + vl * npx;
+            s.dimg = (FWD && s.det_g > 0.0) ? p.det_acc + vl * npx : nullptr;
             s.scale = p.scales + size_t(vc.scale_slot) * npx;
         };
         if (tid >= NT - BK) {
@@ -565,6 +575,8 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
         // shared memory inside that rare branch so no 64-bit address stays
         // live in the cut loop.
         const uint32_t img_slot = sbase + uint32_t(offsetof(Smem, img));
+        const uint32_t dimg_slot = sbase + uint32_t(offsetof(Smem, dimg));
+        const uint32_t detg_slot = sbase + uint32_t(offsetof(Smem, det_g));
         const uint32_t scale_slot = sbase + uint32_t(offsetof(Smem, scale));
         // Each lane carries NV voxels of one column through every cut (NV = NH
         // = 2: the cut record, tile test and loop control are shared
@@ -640,8 +652,15 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                             // zero records (padding row, empty range, mu = 0)
                             // skip the global atomic
                             if (wr != 0.f && v.mu != 0.f) {
-                                float* img = reinterpret_cast<float*>(lds_u64(img_slot));
-                                atomicAdd(img + px, v.mu * r.A * wr);
+                                const float val = v.mu * r.A * wr;
+                                auto* dimg = reinterpret_cast<unsigned long long*>(lds_u64(dimg_slot));
+                                if (dimg) {
+                                    atomicAdd(dimg + px, static_cast<unsigned long long>(
+                                                             __double2ll_rn(double(val) * lds_f64(detg_slot))));
+                                } else {
+                                    float* img = reinterpret_cast<float*>(lds_u64(img_slot));
+                                    atomicAdd(img + px, val);
+                                }
                             }
                         } else {
                             const float* img = reinterpret_cast<const float*>(lds_u64(img_slot));
@@ -734,15 +753,35 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             const int lsh = 31 - __clz(span);             // log2(span)
             const int sub = lane >> lsh, rstep = NWARP << (5 - lsh);
             float* img = s.img + size_t(tm0) * cols + tn0;
-            for (int c0 = 0; c0 < tcols; c0 += span) {
-                const int cc = c0 + (lane & (span - 1));
-                if (cc >= tcols) continue;
-                int* col = itile + cc * tstride;
-                for (int r = (warp << (5 - lsh)) + sub; r < trows; r += rstep) {
-                    const int q = col[r];
-                    if (q != 0) {
-                        col[r] = 0;
-                        atomicAdd(img + size_t(r) * cols + cc, float(q) * inv_qs);
+            if (s.dimg) {
+                // deterministic: the brick's (already order-independent)
+                // int32 tile, rescaled to the launch-wide int64 quantum
+                unsigned long long* dimg = s.dimg + size_t(tm0) * cols + tn0;
+                const double g = s.det_g;
+                for (int c0 = 0; c0 < tcols; c0 += span) {
+                    const int cc = c0 + (lane & (span - 1));
+                    if (cc >= tcols) continue;
+                    int* col = itile + cc * tstride;
+                    for (int r = (warp << (5 - lsh)) + sub; r < trows; r += rstep) {
+                        const int q = col[r];
+                        if (q != 0) {
+                            col[r] = 0;
+                            atomicAdd(dimg + size_t(r) * cols + cc, static_cast<unsigned long long>(
+                                                                        __double2ll_rn(double(float(q) * inv_qs) * g)));
+                        }
+                    }
+                }
+            } else {
+                for (int c0 = 0; c0 < tcols; c0 += span) {
+                    const int cc = c0 + (lane & (span - 1));
+                    if (cc >= tcols) continue;
+                    int* col = itile + cc * tstride;
+                    for (int r = (warp << (5 - lsh)) + sub; r < trows; r += rstep) {
+                        const int q = col[r];
+                        if (q != 0) {
+                            col[r] = 0;
+                            atomicAdd(img + size_t(r) * cols + cc, float(q) * inv_qs);
+                        }
                     }
                 }
             }
@@ -782,6 +821,58 @@ __global__ void apply_scale_kernel(float* __restrict__ out, const float* __restr
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < npx;
          i += size_t(gridDim.x) * blockDim.x)
         o[i] *= __ldg(sc + i);
+}
+
+// Deterministic forward: int64 fixed-point stack -> float32 output with the
+// phase-2 scale (replaces apply_scale_kernel; *g == 0: the float atomics ran).
+__global__ void det_finalize_kernel(float* __restrict__ out, const unsigned long long* __restrict__ acc,
+                                    const double* __restrict__ g, const float* __restrict__ scales,
+                                    const ViewConst* __restrict__ views, int view_begin, size_t npx) {
+    const int v = blockIdx.y;
+    const double gv = *g;
+    const double inv = gv > 0.0 ? 1.0 / gv : 0.0;
+    const float* sc = scales + size_t(views[view_begin + v].scale_slot) * npx;
+    float* o = out + size_t(v) * npx;
+    const unsigned long long* a = acc + size_t(v) * npx;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < npx;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const float val = gv > 0.0 ? float(double(static_cast<long long>(a[i])) * inv) : o[i];
+        o[i] = val * __ldg(sc + i);
+    }
+}
+
+// Launch-wide int64 quantum of the deterministic forward: *g = 2^k with
+// 2^k * bound <= 2^61, bound = max|mu| * factor >= any pixel's pre-scale sum
+// (factor = voxel count * voxel volume / r_min^2: every voxel contributes at
+// most its volume / r_min^2 to one pixel). Non-finite volume: *g = 0.
+template <class T>
+__global__ void det_absmax_kernel(const T* __restrict__ vol, size_t n, unsigned int* maxbits) {
+    float m = 0.f;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const float v = fabsf(float(vol[i]));
+        m = (v != v || m != m) ? __int_as_float(0x7fffffff) : fmaxf(m, v);  // NaN sticks
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float w = __shfl_xor_sync(0xffffffffu, m, o);
+        m = (w != w || m != m) ? __int_as_float(0x7fffffff) : fmaxf(m, w);
+    }
+    // non-negative floats (and the canonical NaN above) order like their bits
+    if ((threadIdx.x & 31) == 0) atomicMax(maxbits, __float_as_uint(m));
+}
+
+__global__ void det_scale_kernel(const unsigned int* maxbits, double factor, double* g) {
+    const float m = __uint_as_float(*maxbits);
+    const double bound = double(m) * factor;
+    if (!isfinite(m) || !isfinite(bound)) {
+        *g = 0.0;
+    } else if (bound == 0.0) {
+        *g = 1.0;
+    } else {
+        int e;
+        frexp(0x1p61 / bound, &e);
+        *g = ldexp(1.0, e - 1);  // power of two <= 2^61 / bound: exact 1/g
+    }
 }
 
 // Per-pixel phase-2 factors (ScaleCache, cvp.cpp:264-302) in float64, stored
@@ -1060,10 +1151,27 @@ cudaError_t CVP_PUB(launch_cvp)(const CvpLaunch& L, cudaStream_t stream) {
     const size_t nvox = size_t(sc.n1) * sc.n2 * sc.n3;
 
     cudaError_t e;
+    const bool det = L.forward && L.det_acc && L.det_g && L.det_maxbits;
     if (L.forward) {
         e = cudaMemsetAsync(L.proj_out, 0, sizeof(float) * npx * L.view_count, stream);
         if (e != cudaSuccess) return e;
     }
+    if (det) {
+        // the quantum from max |mu| over the input (the float64 host volume
+        // when the first chunk reads it in place)
+        e = cudaMemsetAsync(L.det_acc, 0, sizeof(unsigned long long) * npx * L.view_count, stream);
+        if (e == cudaSuccess) e = cudaMemsetAsync(L.det_maxbits, 0, sizeof(unsigned int), stream);
+        if (e != cudaSuccess) return e;
+        if (L.vol_in64)
+            det_absmax_kernel<double><<<148 * 8, 256, 0, stream>>>(L.vol_in64, nvox, L.det_maxbits);
+        else
+            det_absmax_kernel<float><<<148 * 8, 256, 0, stream>>>(L.vol_in, nvox, L.det_maxbits);
+        det_scale_kernel<<<1, 1, 0, stream>>>(L.det_maxbits, 2.0 * L.det_factor, L.det_g);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    p.det_acc = nullptr;
+    p.det_g = det ? L.det_g : nullptr;
     for (int c0 = 0; c0 < L.view_count; c0 += chunk) {
         const int cn = std::min(chunk, L.view_count - c0);
         const int cv0 = L.view_begin + c0;
@@ -1092,6 +1200,7 @@ cudaError_t CVP_PUB(launch_cvp)(const CvpLaunch& L, cudaStream_t stream) {
         p.vol_copy = first ? L.vol_copy : nullptr;
         p.proj_in = L.proj_in ? L.proj_in + size_t(c0) * npx : nullptr;
         p.proj_out = L.proj_out ? L.proj_out + size_t(c0) * npx : nullptr;
+        p.det_acc = det ? L.det_acc + size_t(c0) * npx : nullptr;
         p.accumulate = first ? L.accumulate : 1;
         p.atomic_out = groups > 1 ? 1 : 0;
         // zero-copy float64 output on the last chunk (atomic view groups: convert after)
@@ -1112,8 +1221,12 @@ cudaError_t CVP_PUB(launch_cvp)(const CvpLaunch& L, cudaStream_t stream) {
     }
     if (L.forward) {
         const int bx = int(std::min<size_t>((npx + 255) / 256, 64));
-        apply_scale_kernel<<<dim3(bx, L.view_count), 256, 0, stream>>>(L.proj_out, L.scales, L.views,
-                                                                       L.view_begin, npx);
+        if (det)
+            det_finalize_kernel<<<dim3(bx, L.view_count), 256, 0, stream>>>(
+                L.proj_out, L.det_acc, L.det_g, L.scales, L.views, L.view_begin, npx);
+        else
+            apply_scale_kernel<<<dim3(bx, L.view_count), 256, 0, stream>>>(L.proj_out, L.scales, L.views,
+                                                                           L.view_begin, npx);
         return cudaGetLastError();
     }
     return cudaSuccess;

@@ -4,6 +4,7 @@
 // C-ABI status codes back into the reference's exception types.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <limits>
@@ -74,14 +75,22 @@ cvpb_exec_policy to_c(const ExecPolicy& e) {
 // evicts it meanwhile, plus the entry's mutex for the whole call (a context's
 // host-path buffers, cut-table key and scratch are mutable state). Calls on
 // different scenes run concurrently; calls on one scene serialise.
+//
+// A scene is a multi-device group (cvpb_group, include/cvpb200.h) over every
+// visible GPU — or the devices listed in CBCT_B200_DEVICES ("0,1,2,3", or
+// "0,0" for two members on one GPU) — so an unchanged caller of
+// project_cvp_into / backproject_cvp_into / cgls runs view-sharded on all of
+// them; with one device the group is the single-context path. Siddon-K and
+// the introspection calls run on member 0's context.
 struct SceneEntry {
     cvpb_volume_geometry vol;
     cvpb_detector_geometry det;
     std::vector<cvpb_view> views;
-    cvpb_context* ctx = nullptr;
+    cvpb_group* grp = nullptr;
+    cvpb_context* ctx = nullptr;  // member 0 (owned by the group)
     std::mutex mu;
     ~SceneEntry() {
-        if (ctx) cvpb_context_destroy(ctx);
+        if (grp) cvpb_group_destroy(grp);
     }
 };
 
@@ -90,7 +99,20 @@ struct Lease {
     std::unique_lock<std::mutex> lock;
     cvpb_context* get() const { return entry->ctx; }
     operator cvpb_context*() const { return entry->ctx; }
+    cvpb_group* group() const { return entry->grp; }
 };
+
+// CBCT_B200_DEVICES="i,j,..." -> member devices; empty = every visible device
+std::vector<int> group_devices() {
+    std::vector<int> out;
+    if (const char* env = std::getenv("CBCT_B200_DEVICES")) {
+        std::stringstream ss(env);
+        std::string tok;
+        while (std::getline(ss, tok, ','))
+            if (!tok.empty()) out.push_back(std::stoi(tok));
+    }
+    return out;
+}
 
 std::mutex g_mu;  // guards the LRU list only
 std::list<std::shared_ptr<SceneEntry>> g_scenes;
@@ -125,8 +147,10 @@ Lease scene(const VolumeGeometry& vg, const DetectorGeometry& dg, std::span<cons
         e->vol = v;
         e->det = d;
         e->views = cv;
-        check(cvpb_context_create(0, &e->ctx));
-        check(cvpb_set_geometry(e->ctx, &v, &d, int(cv.size()), cv.data()));
+        const std::vector<int> devs = group_devices();
+        check(cvpb_group_create(devs.empty() ? nullptr : devs.data(), int(devs.size()), &e->grp));
+        check(cvpb_group_set_geometry(e->grp, &v, &d, int(cv.size()), cv.data()));
+        check(cvpb_group_context(e->grp, 0, &e->ctx));
         std::lock_guard<std::mutex> lock(g_mu);
         g_scenes.push_front(e);
         while (g_scenes.size() > 4) g_scenes.pop_back();  // leases keep evicted entries alive
@@ -139,7 +163,9 @@ Lease scene(const VolumeGeometry& vg, const DetectorGeometry& dg, std::span<cons
 Lease any_context() {
     static std::shared_ptr<SceneEntry> e = [] {
         auto p = std::make_shared<SceneEntry>();
-        check(cvpb_context_create(0, &p->ctx));
+        const int dev0 = 0;
+        check(cvpb_group_create(&dev0, 1, &p->grp));
+        check(cvpb_group_context(p->grp, 0, &p->ctx));
         return p;
     }();
     return Lease{e, std::unique_lock<std::mutex>(e->mu)};
@@ -367,8 +393,8 @@ void project_cvp_into(const AttenuationVolume& vol, std::span<const ViewGeometry
     Lease ctx = scene(vol.geom, det, views);
     const cvpb_cvp_options o = to_c(opts);
     const cvpb_exec_policy e = to_c(exec);
-    check(cvpb_project_cvp_host(ctx, &o, &e, vol.values.data(), out.values.data(),
-                                view_seconds ? view_seconds->data() : nullptr));
+    check(cvpb_group_project_cvp_host(ctx.group(), &o, &e, vol.values.data(), out.values.data(),
+                                      view_seconds ? view_seconds->data() : nullptr));
 }
 
 ProjectionStack project_cvp(const AttenuationVolume& vol, std::span<const ViewGeometry> views,
@@ -390,8 +416,8 @@ void backproject_cvp_into(const ProjectionStack& proj, std::span<const ViewGeome
     Lease ctx = scene(vol_geom, proj.det, views);
     const cvpb_cvp_options o = to_c(opts);
     const cvpb_exec_policy e = to_c(exec);
-    check(cvpb_backproject_cvp_host(ctx, &o, &e, proj.values.data(), out.values.data(),
-                                    view_seconds ? view_seconds->data() : nullptr));
+    check(cvpb_group_backproject_cvp_host(ctx.group(), &o, &e, proj.values.data(), out.values.data(),
+                                          view_seconds ? view_seconds->data() : nullptr));
 }
 
 AttenuationVolume backproject_cvp(const ProjectionStack& proj, std::span<const ViewGeometry> views,
@@ -578,7 +604,7 @@ ProjectionStack project_tt(const AttenuationVolume& vol, std::span<const ViewGeo
     ProjectionStack out = ProjectionStack::zeros(det, int(views.size()));
     Lease ctx = scene(vol.geom, det, views);
     const cvpb_tt_options o{int(amp)};
-    check(cvpb_project_tt_host(ctx, &o, vol.values.data(), out.values.data()));
+    check(cvpb_group_project_tt_host(ctx.group(), &o, vol.values.data(), out.values.data()));
     return out;
 }
 
@@ -589,7 +615,7 @@ AttenuationVolume backproject_tt(const ProjectionStack& proj, std::span<const Vi
     AttenuationVolume out = AttenuationVolume::zeros(vol_geom);
     Lease ctx = scene(vol_geom, proj.det, views);
     const cvpb_tt_options o{int(amp)};
-    check(cvpb_backproject_tt_host(ctx, &o, proj.values.data(), out.values.data()));
+    check(cvpb_group_backproject_tt_host(ctx.group(), &o, proj.values.data(), out.values.data()));
     return out;
 }
 
@@ -636,8 +662,8 @@ CglsResult cgls_device(const VolumeGeometry& vol, const DetectorGeometry& det,
     CglsResult res;
     res.x = AttenuationVolume::zeros(vol);
     res.residual_norms.assign(iterations + 1, 0.0);
-    check(cvpb_cgls_host(ctx, 0, &o, nullptr, nullptr, 1, b.values.data(), res.x.values.data(),
-                         iterations, res.residual_norms.data()));
+    check(cvpb_group_cgls_host(ctx.group(), 0, &o, nullptr, nullptr, 1, b.values.data(),
+                               res.x.values.data(), iterations, res.residual_norms.data()));
     return res;
 }
 

@@ -34,6 +34,12 @@ struct CvpLaunch {
     const double* vol_in64 = nullptr;
     float* vol_copy = nullptr;  // forward with vol_in64: also leave a float32 copy here
     double* vol_out64 = nullptr;
+    // forward with ExecPolicy::deterministic: int64 fixed-point merge buffer
+    // (view_count x rows x cols) and scratch for its quantum (det_prepare)
+    unsigned long long* det_acc = nullptr;
+    double* det_g = nullptr;
+    unsigned int* det_maxbits = nullptr;
+    double det_factor = 0.0;  // voxel count * voxel volume / r_min^2 (bound per unit |mu|)
     int* err;                 // device error flag
 };
 
@@ -127,6 +133,18 @@ cudaError_t launch_sart_residual(const float* b, const float* ax, const float* r
                                  size_t n, float eps, cudaStream_t stream);
 cudaError_t launch_sart_update(float* x, const float* corr, const float* colsum, float lambda,
                                int nonneg, size_t n, float eps, cudaStream_t stream);
+// multi-device exchange (group_kernels.cu): out[i] = sum over members h (fixed
+// order, float64) of src.p[h][i] — the z-slab reduce-scatter over peer memory
+constexpr int kMaxMembers = 16;
+struct SlabSources {
+    const float* p[kMaxMembers];
+};
+cudaError_t launch_reduce_slab(const SlabSources& src, int n, size_t count, float* out,
+                               cudaStream_t stream);
+cudaError_t launch_reduce_slab64(const SlabSources& src, int n, size_t count, double* out,
+                                 cudaStream_t stream);
+// error text for the calling thread's cvpb_last_error() (api.cpp)
+int set_last_error(int code, const char* msg);
 cudaError_t launch_f64_to_f32(const double* in, float* out, size_t n, cudaStream_t stream);
 cudaError_t launch_f32_to_f64(const float* in, double* out, size_t n, cudaStream_t stream);
 

@@ -378,6 +378,135 @@ class DeviceScene:
         return x, list(res)
 
 
+class GroupScene:
+    """One scene over several GPUs in this process (libcvpb200 cvpb_group,
+    include/cvpb200.h "multi-device scenes"): views sharded in contiguous
+    ranges, the volume in contiguous z-slabs, the backprojection's partial
+    volumes reduce-scattered over peer memory. ``devices`` may repeat a GPU
+    (``[0, 0]``: two members on one device — the same code path, used to test
+    it on a single-GPU box); None = every visible GPU. Host (float64 numpy)
+    entry points, the reference's call shapes."""
+
+    def __init__(self, vol_geom: VolumeGeometry, det: DetectorGeometry,
+                 views: Sequence[ViewGeometry], devices: Optional[Sequence[int]] = None):
+        L = N.lib()
+        self.vol_geom, self.det = vol_geom, det
+        self.views = list(views)
+        h = C.c_void_p()
+        if devices:
+            arr = (C.c_int * len(devices))(*[int(d) for d in devices])
+            N.check(L.cvpb_group_create(arr, len(devices), C.byref(h)))
+        else:
+            N.check(L.cvpb_group_create(None, 0, C.byref(h)))
+        self._h = h
+        varr = (N.cvpb_view * max(len(self.views), 1))()
+        for i, v in enumerate(self.views):
+            C.memmove(C.byref(varr[i]), C.byref(v._v), C.sizeof(N.cvpb_view))
+        N.check(L.cvpb_group_set_geometry(h, C.byref(vol_geom._c()), C.byref(det._c()),
+                                          len(self.views), varr))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib().cvpb_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def n_views(self):
+        return len(self.views)
+
+    @property
+    def size(self) -> int:
+        n = C.c_int()
+        N.check(N.lib().cvpb_group_size(self._h, C.byref(n)))
+        return n.value
+
+    def member(self, m: int) -> dict:
+        """device, view shard and volume slab (elements) of member m"""
+        d, vb, vc = C.c_int(), C.c_int(), C.c_int()
+        sb, sn = C.c_size_t(), C.c_size_t()
+        N.check(N.lib().cvpb_group_member(self._h, m, C.byref(d), C.byref(vb), C.byref(vc),
+                                          C.byref(sb), C.byref(sn)))
+        return {"device": d.value, "view_begin": vb.value, "view_count": vc.value,
+                "slab_begin": sb.value, "slab_count": sn.value}
+
+    def project_cvp_host(self, vol64, out64=None, opts: CvpOptions = None,
+                         exec: ExecPolicy = None, view_seconds=None):
+        opts = opts or CvpOptions()
+        exec = exec or ExecPolicy()
+        npx = self.det.pixel_count() * self.n_views
+        vol64 = _host64(vol64, self.vol_geom.voxel_count())
+        out64 = np.zeros(npx) if out64 is None else out64
+        _check_host_out(out64, npx)
+        vs = np.zeros(self.n_views) if view_seconds is not None else None
+        N.check(N.lib().cvpb_group_project_cvp_host(
+            self._h, C.byref(opts._c()), C.byref(exec._c()), C.c_void_p(vol64.ctypes.data),
+            C.c_void_p(out64.ctypes.data), C.c_void_p(vs.ctypes.data) if vs is not None else None))
+        if view_seconds is not None:
+            view_seconds[:] = list(vs)
+        return out64
+
+    def backproject_cvp_host(self, proj64, out64=None, opts: CvpOptions = None,
+                             exec: ExecPolicy = None, view_seconds=None):
+        opts = opts or CvpOptions()
+        exec = exec or ExecPolicy()
+        nv = self.vol_geom.voxel_count()
+        proj64 = _host64(proj64, self.det.pixel_count() * self.n_views)
+        out64 = np.zeros(nv) if out64 is None else out64
+        _check_host_out(out64, nv)
+        vs = np.zeros(self.n_views) if view_seconds is not None else None
+        N.check(N.lib().cvpb_group_backproject_cvp_host(
+            self._h, C.byref(opts._c()), C.byref(exec._c()), C.c_void_p(proj64.ctypes.data),
+            C.c_void_p(out64.ctypes.data), C.c_void_p(vs.ctypes.data) if vs is not None else None))
+        if view_seconds is not None:
+            view_seconds[:] = list(vs)
+        return out64
+
+    def project_tt_host(self, vol64, out64=None, opts: TTOptions = None):
+        opts = opts or TTOptions()
+        npx = self.det.pixel_count() * self.n_views
+        vol64 = _host64(vol64, self.vol_geom.voxel_count())
+        out64 = np.zeros(npx) if out64 is None else out64
+        _check_host_out(out64, npx)
+        N.check(N.lib().cvpb_group_project_tt_host(self._h, C.byref(opts._c()),
+                                                   C.c_void_p(vol64.ctypes.data),
+                                                   C.c_void_p(out64.ctypes.data)))
+        return out64
+
+    def backproject_tt_host(self, proj64, out64=None, opts: TTOptions = None):
+        opts = opts or TTOptions()
+        nv = self.vol_geom.voxel_count()
+        proj64 = _host64(proj64, self.det.pixel_count() * self.n_views)
+        out64 = np.zeros(nv) if out64 is None else out64
+        _check_host_out(out64, nv)
+        N.check(N.lib().cvpb_group_backproject_tt_host(self._h, C.byref(opts._c()),
+                                                       C.c_void_p(proj64.ctypes.data),
+                                                       C.c_void_p(out64.ctypes.data)))
+        return out64
+
+    def cgls_host(self, b64, iterations: int, projector: str = "cvp", opts: CvpOptions = None,
+                  tt: TTOptions = None, exec: ExecPolicy = None, k_per_edge: int = 1):
+        """cgls (solver.cpp:55-106) device-resident across the members; returns
+        (x float64, residual norms)."""
+        kind = {"cvp": 0, "siddon": 1, "tt": 2}[projector]
+        opts = opts or CvpOptions()
+        tt = tt or TTOptions()
+        exec = exec or ExecPolicy()
+        b64 = _host64(b64, self.det.pixel_count() * self.n_views)
+        x = np.zeros(self.vol_geom.voxel_count())
+        hist = np.zeros(int(iterations) + 1)
+        N.check(N.lib().cvpb_group_cgls_host(
+            self._h, kind, C.byref(opts._c()), C.byref(tt._c()), C.byref(exec._c()),
+            int(k_per_edge), C.c_void_p(b64.ctypes.data), C.c_void_p(x.ctypes.data),
+            int(iterations), hist.ctypes.data_as(C.POINTER(C.c_double))))
+        return x, hist
+
+
 def _host64(a, n):
     a = np.ascontiguousarray(a, dtype=np.float64).ravel()
     if a.size != n:

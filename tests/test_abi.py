@@ -49,7 +49,7 @@ def test_abi_version_and_no_cpu_fallback():
     import torch
     from paper_2110_09841_b200 import _native
     L = _native.lib()
-    assert L.cvpb_abi_version() == 2
+    assert L.cvpb_abi_version() == 3
     n = C.c_int()
     assert L.cvpb_device_count(C.byref(n)) == 0
     if torch.cuda.is_available():

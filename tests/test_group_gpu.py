@@ -1,0 +1,175 @@
+"""Multi-device scenes (cvpb_group, include/cvpb200.h) on one GPU.
+
+The box has one B200, so the group's members repeat device 0 ([0, 0],
+[0, 0, 0]): every member still gets its own context, stream, host thread,
+view shard and z-slab, the slabs are all-gathered with peer copies and the
+backprojection partials are reduce-scattered by the peer-load kernel — the
+same code an 8-GPU group runs, with the NVLink hop replaced by local HBM.
+
+Bars:
+* forward: each view is projected by exactly one member with the same kernel
+  as the single-context path -> equal to the one-context host path within
+  float32 atomic reassociation (1e-6), and to the reference Double within the
+  north-star bar (rel-L2 1e-5, max 1e-4);
+* backward: partials summed in a fixed member order in float64 -> within
+  float32 reassociation of the one-context result, and within the bar of the
+  reference;
+* CGLS: the residual history of the group equals the single-device
+  device-resident CGLS (rtol 1e-5) and the reference's cgls (rtol 1e-5).
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import make_case, max_rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+THREADS = os.cpu_count() or 1
+
+CASE = ((48, 40, 36), (0.9, 0.9, 0.9), 96, 112, 0.6, 0.6, 160.0, 260.0, 24)
+
+
+def _data(geom, det, nv):
+    import paper_2110_09841_b200 as cb
+    x = cb.fill_uniform01(geom.voxel_count(), 7)
+    b = cb.fill_uniform01(det.pixel_count() * nv, 8)
+    return x, b
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0]])
+def test_group_cvp_matches_single_context_and_reference(devices, reference):
+    import paper_2110_09841_b200 as cb
+    geom, det, views, sc = make_case(*CASE)
+    x, b = _data(geom, det, len(views))
+    grp = cb.GroupScene(geom, det, views, devices=devices)
+    assert grp.size == len(devices)
+    # shards: contiguous views and z-slabs covering everything once
+    vb, sb = 0, 0
+    for m in range(grp.size):
+        info = grp.member(m)
+        assert info["view_begin"] == vb and info["slab_begin"] == sb
+        vb += info["view_count"]
+        sb += info["slab_count"]
+        assert info["slab_count"] % (geom.counts[0] * geom.counts[1]) == 0
+    assert vb == len(views) and sb == geom.voxel_count()
+    one = cb.DeviceScene(geom, det, views)
+    for prec in (cb.CvpPrecision.Double, cb.CvpPrecision.Single):
+        opts = cb.CvpOptions(precision=prec)
+        vs = [0.0] * len(views)
+        p_g = grp.project_cvp_host(x, opts=opts, view_seconds=vs)
+        assert all(t > 0 for t in vs)
+        p_1 = one.project_cvp_host(x, opts=opts)
+        assert rel_l2(p_g, p_1) < 1e-6
+        bp_g = grp.backproject_cvp_host(b, opts=opts)
+        bp_1 = one.backproject_cvp_host(b, opts=opts)
+        assert rel_l2(bp_g, bp_1) < 1e-6
+        p_ref = reference.project_cvp(sc, x, (1, 1, 0, 1), threads=THREADS)
+        bp_ref = reference.backproject_cvp(sc, b, (1, 1, 0, 1), threads=THREADS)
+        assert rel_l2(p_g, p_ref) <= 1e-5 and max_rel(p_g, p_ref) <= 1e-4
+        assert rel_l2(bp_g, bp_ref) <= 1e-5 and max_rel(bp_g, bp_ref) <= 1e-4
+    grp.close()
+    one.close()
+
+
+def test_group_backward_is_deterministic():
+    """Fixed member order in the reduce-scatter: two runs are bit-identical."""
+    import paper_2110_09841_b200 as cb
+    geom, det, views, _ = make_case(*CASE)
+    _, b = _data(geom, det, len(views))
+    grp = cb.GroupScene(geom, det, views, devices=[0, 0])
+    ex = cb.ExecPolicy(deterministic=True)
+    a = grp.backproject_cvp_host(b, exec=ex)
+    c = grp.backproject_cvp_host(b, exec=ex)
+    assert np.array_equal(a, c)
+
+
+def test_group_more_members_than_views():
+    """Members without views (and without z-planes) take part without work."""
+    import paper_2110_09841_b200 as cb
+    geom, det, views, _ = make_case((16, 16, 2), (1.0, 1.0, 1.0), 32, 32, 1.0, 1.0, 60.0, 100.0, 2)
+    x, b = _data(geom, det, 2)
+    grp = cb.GroupScene(geom, det, views, devices=[0, 0, 0])
+    assert [grp.member(m)["view_count"] for m in range(3)] == [0, 1, 1]
+    assert [grp.member(m)["slab_count"] for m in range(3)] == [0, 256, 256]
+    one = cb.DeviceScene(geom, det, views)
+    assert rel_l2(grp.project_cvp_host(x), one.project_cvp_host(x)) < 1e-6
+    assert rel_l2(grp.backproject_cvp_host(b), one.backproject_cvp_host(b)) < 1e-6
+
+
+def test_group_tt_matches_single_context():
+    import paper_2110_09841_b200 as cb
+    geom, det, views, _ = make_case(*CASE)
+    x, b = _data(geom, det, len(views))
+    import torch
+    grp = cb.GroupScene(geom, det, views, devices=[0, 0])
+    one = cb.DeviceScene(geom, det, views)
+    xd = torch.from_numpy(x.astype(np.float32)).reshape(geom.shape()).cuda()
+    bd = torch.from_numpy(b.astype(np.float32)).reshape(len(views), det.rows, det.cols).cuda()
+    p_1 = one.project_tt(xd).double().cpu().numpy().ravel()
+    bp_1 = one.backproject_tt(bd).double().cpu().numpy().ravel()
+    assert rel_l2(grp.project_tt_host(x), p_1) < 1e-6
+    assert rel_l2(grp.backproject_tt_host(b), bp_1) < 1e-6
+
+
+@pytest.mark.parametrize("projector", ["cvp", "tt", "siddon"])
+def test_group_cgls_matches_single_device(projector):
+    import torch
+    import paper_2110_09841_b200 as cb
+    geom, det, views, _ = make_case(*CASE)
+    _, b = _data(geom, det, len(views))
+    grp = cb.GroupScene(geom, det, views, devices=[0, 0, 0])
+    x_g, h_g = grp.cgls_host(b, 6, projector=projector)
+    one = cb.DeviceScene(geom, det, views)
+    bd = torch.from_numpy(b.astype(np.float32)).reshape(len(views), det.rows, det.cols).cuda()
+    x_1, h_1 = one.cgls(bd, 6, projector=projector)
+    np.testing.assert_allclose(h_g, h_1, rtol=1e-5)
+    assert rel_l2(x_g, x_1.double().cpu().numpy().ravel()) < 1e-4
+
+
+def test_group_cgls_matches_reference(reference):
+    import paper_2110_09841_b200 as cb
+    geom, det, views, sc = make_case(*CASE)
+    _, b = _data(geom, det, len(views))
+    grp = cb.GroupScene(geom, det, views, devices=[0, 0])
+    x_g, h_g = grp.cgls_host(b, 8)
+    x_r, h_r = reference.cgls(sc, b, 8, 0, (1, 1, 0, 1))
+    np.testing.assert_allclose(h_g, h_r, rtol=1e-5)
+    assert rel_l2(x_g, x_r.ravel()) < 1e-4
+
+
+def test_group_errors_are_the_reference_exceptions():
+    """A member's failure aborts the others and surfaces with the reference's
+    exception type and message (source inside the volume: cvp.cpp:242-246)."""
+    import paper_2110_09841_b200 as cb
+    from paper_2110_09841_b200._native import CvpbRuntimeError
+    det = cb.DetectorGeometry.make(32, 32, 1.0, 1.0)
+    geom = cb.VolumeGeometry.make((64, 64, 64), (1.0, 1.0, 1.0))
+    views = cb.make_circular_trajectory(20.0, 60.0, 4, 360.0, det)  # source inside the box
+    grp = cb.GroupScene(geom, det, views, devices=[0, 0])
+    with pytest.raises(CvpbRuntimeError, match="source inside the volume box"):
+        grp.project_cvp_host(np.zeros(geom.voxel_count()))
+    with pytest.raises(CvpbRuntimeError, match="source inside the volume box"):
+        grp.backproject_cvp_host(np.zeros(det.pixel_count() * 4))
+
+
+@pytest.mark.parametrize("unit", ["test_cvp", "test_solver"])
+def test_reference_unit_tests_through_a_two_member_group(unit):
+    """The reference's own test_cvp / test_solver, unmodified, with every
+    scene of the drop-in a two-member group (CBCT_B200_DEVICES=0,0): the
+    unchanged C++ caller drives the multi-device path. Same expected float64
+    misses as tests/test_reference_callers_gpu.py."""
+    import re
+    from test_reference_callers_gpu import EXPECTED_PRECISION_MISSES
+    exe = os.path.join(ROOT, "tests", "cpp", "bin", unit)
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (needs /root/reference at build time)")
+    env = dict(os.environ, CBCT_B200_DEVICES="0,0", CBCT_B200_ROOT=ROOT)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=1800, env=env,
+                         cwd=os.path.dirname(exe))
+    cases = re.findall(r"^TEST (.*): (\d+) checks, (\d+) failed$", out.stdout, flags=re.M)
+    assert cases, out.stdout[-2000:] + out.stderr[-2000:]
+    bad = [(n, int(f)) for n, c, f in cases if int(f) and n not in EXPECTED_PRECISION_MISSES]
+    assert not bad, out.stdout[-4000:]

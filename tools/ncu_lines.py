@@ -20,5 +20,6 @@ for rec in csv.reader(out.splitlines()):
         if ins or smp: rows.append((fname, int(rec[0]), ins, smp, rec[1].strip()[:90]))
 ti = sum(r[2] for r in rows); ts = sum(r[3] for r in rows)
 print(f"total warp-instr {ti:.3e}  samples {ts}")
-for r in sorted(rows, key=lambda r: -r[3])[:top]:
+key = 2 if len(sys.argv) > 4 and sys.argv[4] == "ins" else 3
+for r in sorted(rows, key=lambda r: -r[key])[:top]:
     print(f"{r[0]:>18}:{r[1]:<4} ins {100*r[2]/ti:5.1f}%  stall {100*r[3]/ts:5.1f}%  {r[4]}")
