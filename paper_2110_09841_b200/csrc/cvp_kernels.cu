@@ -153,7 +153,8 @@ struct Smem {
     float mu_abs_max;         // forward: max |mu| over the brick
     int nonfinite;            // forward: the brick holds a NaN / Inf attenuation
     float qscale;             // forward: fixed-point scale of this (brick, view)
-    int walk_mode;            // 0: general row walk; 1 / 2: walk_rows_fast<1 / 2>
+    int walk_mode;            // 0: general row walk; 1 / 2: walk_rows_fast<1 / 2>;
+                              // 3 / 4: the same with rows off the detector dropped
 };
 
 // 32-bit shared-window addressing for the hot paths: with 80 registers the
@@ -422,11 +423,17 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                     rho2max = fmaxf(rho2max, x * x + y * y);
                 }
                 const bool gate_ok = !corr || dz_near * dz_near > 4e-28f * rho2max;
-                if (rows_inside && k1 == k0 + BK && dl > 0.f && gate_ok) {
+                if (k1 == k0 + BK && dl > 0.f && gate_ok) {
                     const float dzm = fmaxf(fabsf(zlo), fabsf(zhi));
                     const float rdl = 1.f / dl;
                     const float tr = (0.5f * float(sc.a3) + dzm * ddm / dmin) * fb2 * rdl * 1.0001f + 2e-5f;
                     mode = 2.f * tr < 0.999f ? 1 : 2.f * tr < 1.999f ? 2 : 0;
+                    // a brick whose rows reach past the detector's top or
+                    // bottom edge walks the same rows and drops the records
+                    // of rows off the detector: a row's share depends only
+                    // on its own two boundaries, so this is exactly the
+                    // reference's clamped range (cvp.cpp:197-201)
+                    if (mode && !rows_inside) mode += 2;
                 }
                 s.walk_mode = mode;
             }
@@ -678,22 +685,31 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             auto fast_cut = [&](const CutRec& r, VoxState& v) {
                 // (fast mode: the elevation gate holds for every voxel-cut of
                 // the brick, footprint())
+                constexpr int NB = (MODE == 2 || MODE == 4) ? 2 : 1;
+                constexpr bool CLIP = MODE >= 3;  // rows off the detector: weight 0
                 const float sh = corr ? r.shw : 0.f;
                 const float uh = fmaf(v.dz, r.kc, v.u0h);
                 const uint32_t cbase = tbase + 4u * uint32_t((r.n - tn0) * tstride - tm0);
                 int nrow = 0;
                 auto emit = [&](int m, float w) {
                     uint32_t a = cbase + 4u * uint32_t(m);
-                    if (MODE == 2 && nrow == 2) a = tbase + 4u * min(uint32_t((r.n - tn0) * tstride + m - tm0),
-                                                                    uint32_t((r.n - tn0) * tstride) + trm1);
+                    if (CLIP) {
+                        // every on-detector row lies in the tile (2-row
+                        // margin); the dropped ones write 0 to any tile slot
+                        a = tbase + 4u * (uint32_t((r.n - tn0) * tstride) + min(uint32_t(m - tm0), trm1));
+                        w = unsigned(m) < unsigned(rows) ? w : 0.f;
+                    } else if (NB == 2 && nrow == 2) {
+                        a = tbase + 4u * min(uint32_t((r.n - tn0) * tstride + m - tm0),
+                                             uint32_t((r.n - tn0) * tstride) + trm1);
+                    }
                     ++nrow;
                     if (FWD)
                         red_s32(a, __float2int_rn(w));
                     else
                         v.acc = fmaf(lds_f32(a), w, v.acc);
                 };
-                walk_rows_fast<MODE == 2 ? 2 : 1>(r, v.Mi, uh, v.pmh, v.dz, h, sh, per_row_r,
-                                                  v.inv_r2_fixed, FWD ? v.muq * r.A : r.A, emit);
+                walk_rows_fast<NB>(r, v.Mi, uh, v.pmh, v.dz, h, sh, per_row_r, v.inv_r2_fixed,
+                                   FWD ? v.muq * r.A : r.A, emit);
             };
             auto cut = [&](const CutRec& r) {
                 if (tile_ok && unsigned(r.n - tn0) < unsigned(tcols)) {
@@ -737,8 +753,12 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             const int mode = s.walk_mode;
             if (mode == 1)
                 vphase(std::integral_constant<int, 1>{});
+            else if (mode == 3)
+                vphase(std::integral_constant<int, 3>{});
             else if (mode == 2)
                 vphase(std::integral_constant<int, 2>{});
+            else if (mode == 4)
+                vphase(std::integral_constant<int, 4>{});
             else
                 vphase(std::integral_constant<int, 0>{});
         }
