@@ -288,6 +288,56 @@ __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene
     if (rows_inside) *rows_inside = r0 >= 0 && r1 <= sc.rows - 1;
 }
 
+// Cuts q0 .. q0 + kOverflowCap - 1 of column (i, j) under view *vc — those
+// past the MAXC that the cut table caches — recomputed out of line. Inlined,
+// the float64 column geometry (column_cuts) set the register allocation of
+// the whole V-phase and forced 100-150 B of spills into every kernel variant
+// (reloaded on the hot cut loop); behind a call the rare path pays for its
+// own registers at the call site only.
+constexpr int kOverflowCap = 8;
+template <bool EXACT>
+__device__ __noinline__ void overflow_cuts(const ViewConst* vc, Scene sc, int i, int j, int corr,
+                                           int q0, CutRec* out) {
+    ColumnRec col;
+    int idx = 0;
+    column_cuts<EXACT>(*vc, sc, i, j, true, corr != 0, col, [&](const CutRec& r) {
+        if (idx >= q0 && idx < q0 + kOverflowCap) out[idx - q0] = r;
+        ++idx;
+    });
+}
+
+// One voxel-cut whose column is off the brick's detector tile (tile overflow
+// or a column outside the footprint): records go straight to HBM — float
+// atomics, or the int64 merge stack in deterministic mode — and the backward
+// gathers the scaled image from L2. Out of line for the same reason as
+// overflow_cuts. Returns the backward's sum of image * weight.
+template <bool FWD, int NR>
+__device__ __noinline__ float offtile_walk(CutRec r, int Mi, float Mf, float uh, float pmh, float dz,
+                                           float h, float sh, int per_row_r, float inv_r2_fixed,
+                                           int rows, int cols, float mu, float* img,
+                                           const float* scl, unsigned long long* dimg, double g) {
+    float cut_acc = 0.f;
+    auto emit = [&](int m, float wr) {
+        // the walk's padding emit may sit one row past the detector
+        const size_t px = size_t(min(m, rows - 1)) * cols + r.n;
+        if (FWD) {
+            // zero records (padding row, empty range, mu = 0) skip the atomic
+            if (wr != 0.f && mu != 0.f) {
+                const float val = mu * r.A * wr;
+                if (dimg)
+                    atomicAdd(dimg + px, static_cast<unsigned long long>(__double2ll_rn(double(val) * g)));
+                else
+                    atomicAdd(img + px, val);
+            }
+        } else {
+            cut_acc = fmaf(__ldg(img + px) * __ldg(scl + px), wr, cut_acc);
+        }
+    };
+    walk_rows<true, decltype(emit)&, true, NR>(r, Mi, Mf, uh, pmh, dz, h, sh, per_row_r != 0,
+                                               inv_r2_fixed, rows, emit);
+    return cut_acc;
+}
+
 // CORR: elevation correction option; CCR: CutCentroid radius estimate
 // (cvp.hpp:17-22) — compile-time so the unused paths cost no registers.
 template <bool EXACT, bool FWD, bool CORR, bool CCR, int NR>
@@ -643,38 +693,24 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 const uint32_t cbase = tbase + 4u * uint32_t((r.n - tn0) * tstride);
                 const float wA = FWD ? v.muq * r.A : r.A;
                 float cut_acc = 0.f;
+                if constexpr (!TILE) {
+                    // off the tile (overflow, column outside it): rare, out of line
+                    const float ca = offtile_walk<FWD, NR>(
+                        r, v.Mi, v.Mf, uh, v.pmh, v.dz, h, sh, per_row_r ? 1 : 0, v.inv_r2_fixed,
+                        rows, cols, v.mu, reinterpret_cast<float*>(lds_u64(img_slot)),
+                        reinterpret_cast<const float*>(lds_u64(scale_slot)),
+                        reinterpret_cast<unsigned long long*>(lds_u64(dimg_slot)), lds_f64(detg_slot));
+                    if (!FWD) v.acc = fmaf(wA, ca, v.acc);
+                    return;
+                }
                 auto emit = [&](int m, float wr) {
-                    if (TILE) {
-                        // rows off the tile (either side) carry share 0: any
-                        // in-tile slot will do, so one unsigned min clamps both
-                        const uint32_t a = cbase + 4u * min(uint32_t(m - tm0), trm1);
-                        if (FWD)
-                            red_s32(a, __float2int_rn(wr * wA));
-                        else
-                            cut_acc = fmaf(lds_f32(a), wr, cut_acc);
-                    } else {
-                        // the walk's padding emit may sit one row past the detector
-                        const size_t px = size_t(min(m, rows - 1)) * cols + r.n;
-                        if (FWD) {
-                            // zero records (padding row, empty range, mu = 0)
-                            // skip the global atomic
-                            if (wr != 0.f && v.mu != 0.f) {
-                                const float val = v.mu * r.A * wr;
-                                auto* dimg = reinterpret_cast<unsigned long long*>(lds_u64(dimg_slot));
-                                if (dimg) {
-                                    atomicAdd(dimg + px, static_cast<unsigned long long>(
-                                                             __double2ll_rn(double(val) * lds_f64(detg_slot))));
-                                } else {
-                                    float* img = reinterpret_cast<float*>(lds_u64(img_slot));
-                                    atomicAdd(img + px, val);
-                                }
-                            }
-                        } else {
-                            const float* img = reinterpret_cast<const float*>(lds_u64(img_slot));
-                            const float* scl = reinterpret_cast<const float*>(lds_u64(scale_slot));
-                            cut_acc = fmaf(__ldg(img + px) * __ldg(scl + px), wr, cut_acc);
-                        }
-                    }
+                    // rows off the tile (either side) carry share 0: any
+                    // in-tile slot will do, so one unsigned min clamps both
+                    const uint32_t a = cbase + 4u * min(uint32_t(m - tm0), trm1);
+                    if (FWD)
+                        red_s32(a, __float2int_rn(wr * wA));
+                    else
+                        cut_acc = fmaf(lds_f32(a), wr, cut_acc);
                 };
                 walk_rows<true, decltype(emit)&, true, NR>(r, v.Mi, v.Mf, uh, v.pmh, v.dz, h, sh,
                                                            per_row_r, v.inv_r2_fixed, rows, emit);
@@ -732,15 +768,17 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             if (any_active) {
                 const int ncached = min(cnt, MAXC);
                 for (int q = 0; q < ncached; ++q) cut(load_cut(sbase, q * NCOL + c));
-            }
-            if (cnt > MAXC) {
-                // rare overflow (pixels much smaller than voxels): recompute cuts >= MAXC
-                const int i = i0 + (c % BI), j = j0 + (c / BI);
-                ColumnRec col;
-                int idx = 0;
-                column_cuts<EXACT>(vc, sc, i, j, true, corr, col, [&](const CutRec& r) {
-                    if (idx++ >= MAXC) cut(r);
-                });
+                if (cnt > MAXC) {
+                    // overflow (pixels much smaller than voxels): cuts >= MAXC
+                    // recomputed out of line, kOverflowCap at a time
+                    const int i = i0 + (c % BI), j = j0 + (c / BI);
+                    CutRec extra[kOverflowCap];
+                    for (int q0 = MAXC; q0 < cnt; q0 += kOverflowCap) {
+                        overflow_cuts<EXACT>(&vc, sc, i, j, corr ? 1 : 0, q0, extra);
+                        const int nx = min(cnt - q0, kOverflowCap);
+                        for (int q = 0; q < nx; ++q) cut(extra[q]);
+                    }
+                }
             }
             if (!FWD) {
 #pragma unroll
