@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import platform
 import socket
@@ -509,11 +510,20 @@ def run_native(args):
     sp = (_profile_file("ncu_r02_fwd_summary.txt", "ncu_r01_fwd_summary.txt") if fwd_dom else
           _profile_file("ncu_r02_bwd_summary.txt", "ncu_r01_bwd_summary.txt"))
     if sp:
-        issue = None
+        # the summary may list several kernels: take the dominant direction's
+        # block (FWD: template flag 1, BWD: 0) and only a finite value
+        issue, want, in_block = None, ("<1, 1," if fwd_dom else "<1, 0,"), False
         with open(sp) as f:
             for line in f:
-                if "smsp__issue_active.avg.pct_of_peak_sustained_active" in line:
-                    issue = float(line.split()[-1]) / 100.0
+                if line.startswith("=="):
+                    in_block = want in line
+                elif in_block and "smsp__issue_active.avg.pct_of_peak_sustained_active" in line:
+                    try:
+                        val = float(line.split()[-1]) / 100.0
+                    except ValueError:
+                        continue
+                    if math.isfinite(val) and issue is None:
+                        issue = val
         if issue is not None:
             roofline["issue"] = {"bound": "issue", "frac": issue, "metric": "smsp__issue_active",
                                  "source": os.path.relpath(sp, ROOT) + " (ncu --set full)"}

@@ -171,6 +171,16 @@ int cvpb_backproject_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
                               const cvpb_exec_policy* exec, const double* proj, double* volume,
                               double* view_seconds);
 
+/* view_seconds of the host calls (cvp.cpp:469-477 times each view's loop).
+ * The device runs all views of a launch at once, so a launch's measured time
+ * is attributed to its views in proportion to their work, the number of
+ * voxel-column cuts each view has; this returns those weights for views
+ * [view_begin, view_begin + view_count) (normalized to sum 1; equal weights
+ * when no view has a cut). Builds the range's cut table when it is not
+ * resident. Synchronous on the context's stream. */
+int cvpb_cvp_view_weights(cvpb_context* ctx, const cvpb_cvp_options* opts, int view_begin,
+                          int view_count, double* weights);
+
 /* Multi-GPU building blocks of the host path (one rank per GPU, views
  * sharded: each rank's context holds its own view subset). The backward of
  * the host stack with the float32 partial volume left in d_volume (no D2H):

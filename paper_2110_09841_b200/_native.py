@@ -79,6 +79,7 @@ SIGNATURES = {
                                         _vp, _vp]),
     "cvpb_backproject_cvp_host": (C.c_int, [_vp, _P(cvpb_cvp_options), _P(cvpb_exec_policy), _vp,
                                             _vp, _vp]),
+    "cvpb_cvp_view_weights": (C.c_int, [_vp, _P(cvpb_cvp_options), C.c_int, C.c_int, _dp]),
     "cvpb_collect_cut_records": (C.c_int, [_vp, _P(cvpb_cvp_options), C.c_int, C.c_int, C.c_int,
                                            C.c_int, C.c_int, C.c_int, _ip, _ip, _dp, _dp, _ip]),
     "cvpb_scale_image": (C.c_int, [_vp, C.c_int, C.c_int, _dp]),

@@ -233,6 +233,7 @@ struct cvpb_context {
     DevBuf<double> cg_partials, cg_hist;
     DevBuf<cvpb::CgState> cg_state;
     DevBuf<unsigned long long> d_det;  // deterministic forward: int64 merge stack
+    DevBuf<unsigned long long> d_view_work;  // view_seconds weights (cut counts per view)
     DevBuf<double> d_det_g;
     DevBuf<unsigned int> d_det_max;
     DevBuf<int> d_rec_i;
@@ -664,6 +665,7 @@ void cvpb_context_destroy(cvpb_context* ctx) {
     ctx->d_cut_table.release();
     ctx->d_rec_i.release();
     ctx->d_det.release();
+    ctx->d_view_work.release();
     ctx->d_det_g.release();
     ctx->d_det_max.release();
     ctx->d_rec_d.release();
@@ -956,6 +958,49 @@ int cvpb_backproject_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts,
                    view_count, accumulate, static_cast<cudaStream_t>(stream));
 }
 
+int cvpb_cvp_view_weights(cvpb_context* ctx, const cvpb_cvp_options* opts, int view_begin,
+                          int view_count, double* weights) {
+    CVPB_TRY(check_ctx(ctx));
+    CVPB_TRY(check_cvp_options(opts));
+    CVPB_TRY(check_range(ctx, view_begin, view_count));
+    if (view_count > 0 && !weights) return fail(CVPB_INVALID_ARGUMENT, "null output");
+    if (view_count <= 0) return CVPB_OK;
+    cudaStream_t st = ctx->stream;
+    CVPB_TRY(prepare_cut_table(ctx, opts, view_begin, view_count, st));
+    const auto& key = ctx->cut_key;
+    const int corr = opts->elevation_correction ? 1 : 0;
+    std::vector<unsigned long long> w(size_t(view_count), 0ull);
+    if (key.valid && key.view_begin <= view_begin && view_begin + view_count <= key.view_begin + key.view_count &&
+        key.corr == corr) {
+        CVPB_CUDA(ctx->d_view_work.reserve(size_t(view_count)));
+        if (ctx->ev_table_recorded) CVPB_CUDA(cudaStreamWaitEvent(st, ctx->ev_table, 0));
+        CVPB_CUDA(cvpb::launch_view_work(ctx->d_cut_table.p, ctx->sc.n1 * ctx->sc.n2, key.view_begin,
+                                         key.view_count, view_begin, view_count, ctx->d_view_work.p, st));
+        CVPB_CUDA(cudaEventRecord(ctx->ev_table, st));
+        ctx->ev_table_recorded = true;
+        CVPB_CUDA(cudaMemcpyAsync(w.data(), ctx->d_view_work.p, sizeof(unsigned long long) * view_count,
+                                  cudaMemcpyDeviceToHost, st));
+        CVPB_CUDA(cudaStreamSynchronize(st));
+    }
+    // (a range whose table does not fit in one piece: equal weights)
+    double sum = 0.0;
+    for (unsigned long long x : w) sum += double(x);
+    for (int v = 0; v < view_count; ++v) weights[v] = sum > 0.0 ? double(w[v]) / sum : 1.0 / view_count;
+    return CVPB_OK;
+}
+
+namespace {
+// view_seconds of a host call: the call's measured time (ev0 .. ev1)
+// attributed to the views by cvpb_cvp_view_weights.
+int fill_view_seconds(cvpb_context* ctx, const cvpb_cvp_options* opts, int nviews, double* view_seconds) {
+    float ms = 0.f;
+    CVPB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    CVPB_TRY(cvpb_cvp_view_weights(ctx, opts, 0, nviews, view_seconds));
+    for (int v = 0; v < nviews; ++v) view_seconds[v] *= ms * 1e-3;
+    return CVPB_OK;
+}
+}  // namespace
+
 int cvpb_project_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
                           const cvpb_exec_policy* exec, const double* volume, double* proj,
                           double* view_seconds) {
@@ -995,11 +1040,7 @@ int cvpb_project_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
     CVPB_CUDA(cudaStreamWaitEvent(st, ctx->ev_copy, 0));
     CVPB_CUDA(cudaEventRecord(ctx->ev1, st));
     CVPB_TRY(device_error(ctx, st));
-    if (view_seconds) {
-        float ms = 0.f;
-        CVPB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-        for (int v = 0; v < nviews; ++v) view_seconds[v] = ms * 1e-3 / std::max(nviews, 1);
-    }
+    if (view_seconds) CVPB_TRY(fill_view_seconds(ctx, opts, nviews, view_seconds));
     return CVPB_OK;
 }
 
@@ -1042,11 +1083,7 @@ int cvpb_backproject_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
     }
     CVPB_CUDA(cudaEventRecord(ctx->ev1, st));
     CVPB_TRY(device_error(ctx, st));
-    if (view_seconds) {
-        float ms = 0.f;
-        CVPB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-        for (int v = 0; v < nviews; ++v) view_seconds[v] = ms * 1e-3 / std::max(nviews, 1);
-    }
+    if (view_seconds) CVPB_TRY(fill_view_seconds(ctx, opts, nviews, view_seconds));
     return CVPB_OK;
 }
 

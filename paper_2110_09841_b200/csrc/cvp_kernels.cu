@@ -1300,6 +1300,33 @@ cudaError_t launch_cut_table(const CvpLaunch& L, cudaStream_t stream) {
                          L.exact, L.elevation_correction, L.err, stream);
 }
 
+namespace {
+// one CTA row per view: sum of the per-column cut counts (view_seconds weights)
+__global__ void view_work_kernel(const int* __restrict__ count, int ncols, int vl0,
+                                 unsigned long long* work) {
+    const int v = blockIdx.y;
+    const int* c = count + size_t(vl0 + v) * ncols;
+    unsigned long long s = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ncols; i += gridDim.x * blockDim.x)
+        s += unsigned(max(c[i], 0));
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(work + v, s);
+}
+}  // namespace
+
+cudaError_t launch_view_work(void* cut_table, int ncols, int table_v0, int table_nv, int view_begin,
+                             int view_count, unsigned long long* work, cudaStream_t stream) {
+    if (view_count <= 0) return cudaSuccess;
+    if (!cut_table || view_begin < table_v0 || view_begin + view_count > table_v0 + table_nv)
+        return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(work, 0, sizeof(unsigned long long) * view_count, stream);
+    if (e != cudaSuccess) return e;
+    const CutTable t = cut_table_layout(cut_table, ncols, table_v0, table_nv);
+    const int bx = std::min((ncols + 255) / 256, 16);
+    view_work_kernel<<<dim3(bx, view_count), 256, 0, stream>>>(t.count, ncols, view_begin - table_v0, work);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_scale_image(double f, double pp1, double pp2, double b1, double b2, int rows,
                                int cols, int exact, float* out, double* out64, cudaStream_t stream) {
     const int n = rows * cols;

@@ -315,12 +315,21 @@ int ensure_buffers(cvpb_group* g, int i, int need) {
     return CVPB_OK;
 }
 
-void fill_view_seconds(cvpb_group* g, double* view_seconds, const std::vector<double>& secs) {
-    if (!view_seconds) return;
+// view_seconds (cvp.cpp:469-477): each member's measured time attributed to
+// its views — CVP by their work (cvpb_cvp_view_weights), others equally.
+int fill_view_seconds(cvpb_group* g, const Op& op, double* view_seconds, const std::vector<double>& secs) {
+    if (!view_seconds) return CVPB_OK;
     for (size_t i = 0; i < g->m.size(); ++i) {
         const auto& mb = g->m[i];
-        for (int v = mb.v0; v < mb.v0 + mb.nv; ++v) view_seconds[v] = secs[i] / std::max(mb.nv, 1);
+        if (mb.nv == 0) continue;
+        if (op.kind == 0) {
+            G_TRY(cvpb_cvp_view_weights(mb.ctx, &op.cvp, mb.v0, mb.nv, view_seconds + mb.v0));
+            for (int v = mb.v0; v < mb.v0 + mb.nv; ++v) view_seconds[v] *= secs[i];
+        } else {
+            for (int v = mb.v0; v < mb.v0 + mb.nv; ++v) view_seconds[v] = secs[i] / mb.nv;
+        }
     }
+    return CVPB_OK;
 }
 
 int forward_host(cvpb_group* g, const Op& op, const double* volume, double* proj, double* view_seconds) {
@@ -339,8 +348,7 @@ int forward_host(cvpb_group* g, const Op& op, const double* volume, double* proj
         secs[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         return CVPB_OK;
     }));
-    fill_view_seconds(g, view_seconds, secs);
-    return CVPB_OK;
+    return fill_view_seconds(g, op, view_seconds, secs);
 }
 
 int backward_host(cvpb_group* g, const Op& op, const double* proj, double* volume, double* view_seconds) {
@@ -361,8 +369,7 @@ int backward_host(cvpb_group* g, const Op& op, const double* proj, double* volum
         secs[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         return CVPB_OK;
     }));
-    fill_view_seconds(g, view_seconds, secs);
-    return CVPB_OK;
+    return fill_view_seconds(g, op, view_seconds, secs);
 }
 
 // cgls (solver.cpp:55-106) across the members; see the file comment.

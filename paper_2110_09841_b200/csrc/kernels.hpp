@@ -57,6 +57,12 @@ cudaError_t launch_cvp_c(const CvpLaunch& L, cudaStream_t stream);
 // Only the cut table of views [L.view_begin, L.view_begin + L.view_count)
 // (must fit L.cut_table_bytes); later launches over subsets reuse it.
 cudaError_t launch_cut_table(const CvpLaunch& L, cudaStream_t stream);
+// Per-view work of a launch: the number of voxel-column cuts of views
+// [view_begin, view_begin + view_count) in the resident cut table of views
+// [table_v0, table_v0 + table_nv), one sum per view into work[0..view_count)
+// (zeroed here). view_seconds attributes a launch's time by it.
+cudaError_t launch_view_work(void* cut_table, int ncols, int table_v0, int table_nv, int view_begin,
+                             int view_count, unsigned long long* work, cudaStream_t stream);
 // bytes of cut table per (view, voxel column): count, Q0, rho2c, MAXC x 2 float4
 #ifndef CVP_MAXC
 #define CVP_MAXC 4

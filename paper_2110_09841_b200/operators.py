@@ -240,6 +240,16 @@ class DeviceScene:
             view_seconds[:] = list(vs)
         return out64
 
+    def cvp_view_weights(self, opts: CvpOptions = None, view_begin=0, view_count=None) -> np.ndarray:
+        """Per-view share of a CVP launch's work (cut counts, sum 1): how the
+        host calls split their measured time into view_seconds."""
+        opts = opts or CvpOptions()
+        vb, vc = self._range(view_begin, view_count)
+        w = np.zeros(max(vc, 1))
+        N.check(N.lib().cvpb_cvp_view_weights(self._h, C.byref(opts._c()), vb, vc,
+                                              C.c_void_p(w.ctypes.data)))
+        return w[:vc]
+
     def collect_cut_records(self, opts: CvpOptions, view: int, i: int, j: int, k: int,
                             clamp=False, cap=256) -> List[CutVolumeRecord]:
         rows = (C.c_int * cap)()

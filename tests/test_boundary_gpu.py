@@ -95,3 +95,33 @@ def test_device_cgls_flat_history_and_breakdown():
     b[:, 0, 0] = 1.0  # detector corner: outside every footprint of this scene
     x, res = scene.cgls(b, 3)
     assert res[1:] == [res[0]] * 3
+
+
+def test_view_seconds_attribute_the_call_time_by_view_work():
+    """view_seconds (cvp.cpp:469-477): the device runs a launch's views at
+    once, so the call's time is split by each view's cut count. On a slab
+    volume (wide in x1, thin in x2) a view looking along x1 sees fewer
+    columns' cuts than one looking along x2: the weights must differ and sum
+    to one, and both host calls must split their time by them."""
+    import paper_2110_09841_b200 as cb
+    det = cb.DetectorGeometry.make(64, 96, 1.0, 1.0)
+    geom = cb.VolumeGeometry.make((48, 8, 16), (1.0, 1.0, 1.0))
+    views = cb.make_circular_trajectory(120.0, 200.0, 8, 360.0, det)
+    sc = cb.DeviceScene(geom, det, views)
+    opts = cb.CvpOptions()
+    w = sc.cvp_view_weights(opts)
+    assert w.shape == (8,) and np.all(w > 0) and abs(w.sum() - 1.0) < 1e-12
+    assert w.max() / w.min() > 1.5  # 0 deg (along x1) vs 90 deg (along x2)
+    x = cb.fill_uniform01(geom.voxel_count(), 3)
+    vs = [0.0] * 8
+    sc.project_cvp_host(x, opts=opts, view_seconds=vs)
+    vs = np.array(vs)
+    assert np.all(vs > 0)
+    np.testing.assert_allclose(vs / vs.sum(), w, rtol=1e-9)
+    vb = [0.0] * 8
+    sc.backproject_cvp_host(sc.project_cvp_host(x, opts=opts), opts=opts, view_seconds=vb)
+    np.testing.assert_allclose(np.array(vb) / sum(vb), w, rtol=1e-9)
+    # sub-range weights are the range's own shares
+    w2 = sc.cvp_view_weights(opts, view_begin=2, view_count=3)
+    np.testing.assert_allclose(w2, w[2:5] / w[2:5].sum(), rtol=1e-12)
+    sc.close()
