@@ -481,7 +481,11 @@ __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh
             I = mul2(make_float2(fast_rcp(Q.x), fast_rcp(Q.y)), make_float2(wscale, wscale));
         }
         const float2 S = add2(make_float2(h, h), make_float2(-t1, t1));
-        const float2 W = mul2(make_float2(fmaxf(S.x, 0.f), fmaxf(S.y, 0.f)), I);
+        // |t1| <= h: clamp_mean_local is clamp(alpha) plus a correction of
+        // the sign that pulls it inward, so both shares are >= 0 without a
+        // max(., 0) (rounding can leave -ulp(h), far below the fixed-point
+        // quantum; c3 +2% P / BP)
+        const float2 W = mul2(S, I);
         emit(m_first, W.x);
         emit(m_first + 1, W.y);
     } else {

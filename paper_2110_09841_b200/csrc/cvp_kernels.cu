@@ -86,7 +86,7 @@ static_assert(NH % NV == 0, "whole voxel groups per column");
 // Per-lane state of one voxel in the V-phase.
 struct VoxState {
     int Mi;
-    float Mf, u0h, pmh, dz, dz2e28, mu, muq, inv_r2_fixed, acc;
+    float u0h, pmh, dz, dz2e28, mu, muq, inv_r2_fixed, acc;  // (row as float: float(Mi), exact)
     uint32_t vaddr;
     bool kvalid, active;
 };
@@ -667,7 +667,8 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 v.active = v.kvalid && (!FWD || v.mu != 0.f);
                 any_active |= v.active;
                 float u0, pm;
-                anchor_at(an, pp2f, float(kk), v.Mi, v.Mf, u0, pm);
+                float Mf;  // == float(v.Mi) exactly: not kept (one register per voxel)
+                anchor_at(an, pp2f, float(kk), v.Mi, Mf, u0, pm);
                 v.u0h = u0 + 0.5f;
                 v.pmh = pm + 0.5f;
                 v.muq = v.mu * qs;  // forward: fixed-point scale folded into mu
@@ -696,7 +697,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 if constexpr (!TILE) {
                     // off the tile (overflow, column outside it): rare, out of line
                     const float ca = offtile_walk<FWD, NR>(
-                        r, v.Mi, v.Mf, uh, v.pmh, v.dz, h, sh, per_row_r ? 1 : 0, v.inv_r2_fixed,
+                        r, v.Mi, float(v.Mi), uh, v.pmh, v.dz, h, sh, per_row_r ? 1 : 0, v.inv_r2_fixed,
                         rows, cols, v.mu, reinterpret_cast<float*>(lds_u64(img_slot)),
                         reinterpret_cast<const float*>(lds_u64(scale_slot)),
                         reinterpret_cast<unsigned long long*>(lds_u64(dimg_slot)), lds_f64(detg_slot));
@@ -712,7 +713,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                     else
                         cut_acc = fmaf(lds_f32(a), wr, cut_acc);
                 };
-                walk_rows<true, decltype(emit)&, true, NR>(r, v.Mi, v.Mf, uh, v.pmh, v.dz, h, sh,
+                walk_rows<true, decltype(emit)&, true, NR>(r, v.Mi, float(v.Mi), uh, v.pmh, v.dz, h, sh,
                                                            per_row_r, v.inv_r2_fixed, rows, emit);
                 if (!FWD) v.acc = fmaf(wA, cut_acc, v.acc);
             };
@@ -744,8 +745,8 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                     else
                         v.acc = fmaf(lds_f32(a), w, v.acc);
                 };
-                walk_rows_fast<NB>(r, v.Mi, uh, v.pmh, v.dz, h, sh, per_row_r, v.inv_r2_fixed,
-                                   FWD ? v.muq * r.A : r.A, emit);
+                const float ws = FWD ? v.muq * r.A : r.A;
+                walk_rows_fast<NB>(r, v.Mi, uh, v.pmh, v.dz, h, sh, per_row_r, v.inv_r2_fixed, ws, emit);
             };
             auto cut = [&](const CutRec& r) {
                 if (tile_ok && unsigned(r.n - tn0) < unsigned(tcols)) {

@@ -247,7 +247,7 @@ class DeviceScene:
         vb, vc = self._range(view_begin, view_count)
         w = np.zeros(max(vc, 1))
         N.check(N.lib().cvpb_cvp_view_weights(self._h, C.byref(opts._c()), vb, vc,
-                                              C.c_void_p(w.ctypes.data)))
+                                              w.ctypes.data_as(C.POINTER(C.c_double))))
         return w[:vc]
 
     def collect_cut_records(self, opts: CvpOptions, view: int, i: int, j: int, k: int,

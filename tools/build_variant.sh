@@ -13,5 +13,5 @@ F="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -
   || (cat $O/cvp_kernels_$name.ptxas.txt; false)
 /usr/local/cuda/bin/nvcc $F "$@" -x cu -c api.cpp -o $O/api_$name.o 2> /dev/null
 /usr/local/cuda/bin/nvcc -shared -gencode arch=compute_100a,code=sm_100a -cudart static -o ../../build/variants/libcvpb200_$name.so \
-  $O/cvp_kernels_$name.o $B/cvp_kernels_b.o $B/cvp_kernels_c.o $B/siddon_kernels.o $B/tt_kernels.o $B/vecops.o $O/api_$name.o
+  $O/cvp_kernels_$name.o $B/cvp_kernels_b.o $B/cvp_kernels_c.o $B/siddon_kernels.o $B/tt_kernels.o $B/vecops.o $O/api_$name.o $B/group.o $B/group_kernels.o
 grep -A2 "cvp_brick_kernelILb1ELb[01]ELb1ELb1ELi2E" $O/cvp_kernels_$name.ptxas.txt | grep -E "registers|spill"
