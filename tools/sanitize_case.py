@@ -22,3 +22,20 @@ p = scene.project_siddon(x, 2)
 b = scene.backproject_siddon(p, 2)
 torch.cuda.synchronize()
 print("sanitize case ok")
+
+# round 2: the default (non-deterministic) forward — float-atomic flush,
+# virtual tile rows for bricks crossing the detector's top / bottom edge (the
+# volume is taller than the detector's field of view) — and a two-member
+# multi-device group on one GPU (peer all-gather and peer-load reduction)
+for prec in (cb.CvpPrecision.Double, cb.CvpPrecision.Single):
+    o = cb.CvpOptions(precision=prec)
+    p = scene.project_cvp(x, opts=o)
+    b = scene.backproject_cvp(p, opts=o)
+import numpy as np
+grp = cb.GroupScene(geom, det, views, devices=[0, 0])
+x64 = x.double().cpu().numpy().ravel()
+pg = grp.project_cvp_host(x64)
+bg = grp.backproject_cvp_host(pg)
+grp.close()
+torch.cuda.synchronize()
+print("sanitize case (round 2 paths) ok")
