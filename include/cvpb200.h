@@ -163,6 +163,25 @@ int cvpb_backproject_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts,
                          const cvpb_exec_policy* exec, const float* d_proj, float* d_volume,
                          int view_begin, int view_count, int accumulate, void* stream);
 
+/* Backprojection fused with the reduce-scatter of a view-sharded job (SURVEY
+ * §8e): each brick's accumulated voxels are added with float atomics straight
+ * into the buffer that owns their z-plane — typically another GPU's memory,
+ * reached over NVLink peer access — as soon as the brick has walked its
+ * views, so the exchange overlaps the bricks still computing and no partial
+ * volume is materialized. Planes [plane_begin[t], plane_begin[t+1]) go to
+ * slab[t] (its element 0 is the first voxel of plane plane_begin[t]);
+ * plane_begin[0] = 0, plane_begin[n] = N3. The caller zeroes the slabs (or
+ * holds sums to add to) and orders them against this stream. The atomic
+ * order varies run to run: ExecPolicy::deterministic is refused. */
+typedef struct cvpb_slab_targets {
+    int n; /* 1..16 */
+    int plane_begin[17];
+    float* slab[16];
+} cvpb_slab_targets;
+int cvpb_backproject_cvp_scatter(cvpb_context* ctx, const cvpb_cvp_options* opts,
+                                 const cvpb_exec_policy* exec, const float* d_proj, int view_begin,
+                                 int view_count, const cvpb_slab_targets* targets, void* stream);
+
 /* ---- CVP — reference-facing host path (float64 host buffers, H2D/D2H inside) */
 int cvpb_project_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
                           const cvpb_exec_policy* exec, const double* volume, double* proj,

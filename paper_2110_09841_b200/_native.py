@@ -38,6 +38,10 @@ class cvpb_exec_policy(C.Structure):
     _fields_ = [("threads", C.c_int), ("deterministic", C.c_int), ("allow_expensive", C.c_int)]
 
 
+class cvpb_slab_targets(C.Structure):
+    _fields_ = [("n", C.c_int), ("plane_begin", C.c_int * 17), ("slab", C.c_void_p * 16)]
+
+
 class cvpb_pixel_roi(C.Structure):
     _fields_ = [("row_begin", C.c_int), ("row_end", C.c_int), ("col_begin", C.c_int),
                 ("col_end", C.c_int)]
@@ -79,6 +83,8 @@ SIGNATURES = {
                                         _vp, _vp]),
     "cvpb_backproject_cvp_host": (C.c_int, [_vp, _P(cvpb_cvp_options), _P(cvpb_exec_policy), _vp,
                                             _vp, _vp]),
+    "cvpb_backproject_cvp_scatter": (C.c_int, [_vp, _P(cvpb_cvp_options), _P(cvpb_exec_policy), _vp,
+                                               C.c_int, C.c_int, _P(cvpb_slab_targets), _vp]),
     "cvpb_cvp_view_weights": (C.c_int, [_vp, _P(cvpb_cvp_options), C.c_int, C.c_int, _dp]),
     "cvpb_collect_cut_records": (C.c_int, [_vp, _P(cvpb_cvp_options), C.c_int, C.c_int, C.c_int,
                                            C.c_int, C.c_int, C.c_int, _ip, _ip, _dp, _dp, _ip]),

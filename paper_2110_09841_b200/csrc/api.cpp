@@ -349,7 +349,8 @@ cudaError_t launch_cvp_shape(const cvpb::CvpLaunch& L, int shape, cudaStream_t s
 int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_policy* exec,
             bool forward, const float* vol_in, float* vol_out, const float* proj_in,
             float* proj_out, int view_begin, int view_count, int accumulate, cudaStream_t st,
-            const double* vol_in64 = nullptr, double* vol_out64 = nullptr) {
+            const double* vol_in64 = nullptr, double* vol_out64 = nullptr,
+            const cvpb::SlabTargets* targets = nullptr) {
     CVPB_TRY(check_ctx(ctx));
     CVPB_TRY(check_cvp_options(opts));
     CVPB_TRY(check_range(ctx, view_begin, view_count));
@@ -399,6 +400,7 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     L.vol_copy = vol_in64 ? const_cast<float*>(vol_in) : nullptr;
     L.vol_out64 = vol_out64;
     L.err = ctx->d_err.p;
+    if (targets) L.targets = *targets;
     if (forward && L.deterministic && view_count > 0) {
         // bricks merge in int64 fixed point (order-independent): P is
         // bit-reproducible like the reference's deterministic ExecPolicy
@@ -412,6 +414,7 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
         const double vv = ctx->vol.voxel_size[0] * ctx->vol.voxel_size[1] * ctx->vol.voxel_size[2];
         L.det_factor = double(ctx->nvox()) * vv / std::max(ctx->r_min * ctx->r_min, 1e-300);
     }
+    if (!forward && view_count == 0 && (accumulate || targets)) return CVPB_OK;
     if (!forward && view_count == 0 && !accumulate) {
         CVPB_CUDA(cudaMemsetAsync(vol_out, 0, sizeof(float) * ctx->nvox(), st));
         return CVPB_OK;
@@ -430,7 +433,7 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     if (forced) {
         shape = std::min(std::max(std::atoi(forced), 0), 2);
     } else if (it == ctx->cvp_shape.end() && view_count >= 8 && (forward || !accumulate) &&
-               !vol_in64 && !vol_out64) {
+               !vol_in64 && !vol_out64 && !targets) {
         // the timing launches need the whole range's cut table resident
         if (!L.cut_table_valid) {
             CVPB_TRY(prepare_cut_table(ctx, opts, view_begin, view_count, st));
@@ -1000,6 +1003,38 @@ int fill_view_seconds(cvpb_context* ctx, const cvpb_cvp_options* opts, int nview
     return CVPB_OK;
 }
 }  // namespace
+
+int cvpb_backproject_cvp_scatter(cvpb_context* ctx, const cvpb_cvp_options* opts,
+                                 const cvpb_exec_policy* exec, const float* d_proj, int view_begin,
+                                 int view_count, const cvpb_slab_targets* targets, void* stream) {
+    CVPB_TRY(check_ctx(ctx));
+    if (!targets) return fail(CVPB_INVALID_ARGUMENT, "null slab targets");
+    if (exec && exec->deterministic)
+        return fail(CVPB_INVALID_ARGUMENT,
+                    "the fused reduce-scatter adds with atomics: not bit-reproducible "
+                    "(use cvpb_backproject_cvp + a fixed-order reduction for ExecPolicy::deterministic)");
+    const int n = targets->n;
+    if (n < 1 || n > cvpb::kMaxSlabTargets)
+        return fail(CVPB_INVALID_ARGUMENT, "slab targets: 1 to 16 slabs");
+    const int n3 = ctx->vol.counts[2];
+    if (targets->plane_begin[0] != 0 || targets->plane_begin[n] != n3)
+        return fail(CVPB_INVALID_ARGUMENT, "slab targets must cover the volume's planes [0, N3)");
+    cvpb::SlabTargets tg;
+    tg.n = n;
+    for (int t = 0; t <= n; ++t) {
+        if (t > 0 && targets->plane_begin[t] < targets->plane_begin[t - 1])
+            return fail(CVPB_INVALID_ARGUMENT, "slab target planes must not decrease");
+        tg.plane_begin[t] = targets->plane_begin[t];
+    }
+    for (int t = 0; t < n; ++t) {
+        if (!targets->slab[t] && targets->plane_begin[t + 1] > targets->plane_begin[t])
+            return fail(CVPB_INVALID_ARGUMENT, "null slab target");
+        tg.slab[t] = targets->slab[t];
+    }
+    if (!d_proj && view_count > 0) return fail(CVPB_INVALID_ARGUMENT, "null projection buffer");
+    return run_cvp(ctx, opts, exec, false, nullptr, nullptr, d_proj, nullptr, view_begin, view_count, 1,
+                   static_cast<cudaStream_t>(stream), nullptr, nullptr, &tg);
+}
 
 int cvpb_project_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,
                           const cvpb_exec_policy* exec, const double* volume, double* proj,

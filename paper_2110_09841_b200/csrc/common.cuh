@@ -34,6 +34,17 @@ struct Scene {
     double pw, ph;
 };
 
+// Backprojection fused with a reduce-scatter (cvpb_backproject_cvp_scatter):
+// planes [plane_begin[t], plane_begin[t + 1]) of the volume go to slab[t]
+// (element 0 = first voxel of plane plane_begin[t]), added with atomics —
+// slab[t] may live in another GPU's memory (peer access).
+constexpr int kMaxSlabTargets = 16;
+struct SlabTargets {
+    int n = 0;
+    int plane_begin[kMaxSlabTargets + 1] = {};
+    float* slab[kMaxSlabTargets] = {};
+};
+
 // Error flags raised by kernels (checked by the host after the launch).
 enum DeviceError : int {
     kDevOk = 0,

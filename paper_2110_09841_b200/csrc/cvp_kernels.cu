@@ -131,6 +131,7 @@ struct CvpParams {
     // (non-finite volume) falls back to the float atomics
     unsigned long long* det_acc;
     const double* det_g;
+    SlabTargets tg;           // backward fused with a reduce-scatter (tg.n > 0)
     int* err;
 };
 
@@ -877,8 +878,17 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             const int i = i0 + (c % BI), j = j0 + (c / BI), kq = k0 + kk;
             if (i < i1 && j < j1 && kq < k1) {
                 const size_t off = size_t(kq) * plane + size_t(j) * sc.n1 + i;
-                float* dst = p.vol_out + off;
                 const float val = s.vox[c * MUS + kk];
+                if (p.tg.n > 0) {
+                    // fused reduce-scatter: straight into the slab that owns
+                    // plane kq (another GPU's memory over NVLink), while the
+                    // other bricks are still computing
+                    int t = 0;
+                    while (t + 1 < p.tg.n && kq >= p.tg.plane_begin[t + 1]) ++t;
+                    atomicAdd(p.tg.slab[t] + (off - size_t(p.tg.plane_begin[t]) * plane), val);
+                    continue;
+                }
+                float* dst = p.vol_out + off;
                 if (p.atomic_out) {
                     atomicAdd(dst, val);
                 } else {
@@ -1218,6 +1228,7 @@ cudaError_t CVP_PUB(launch_cvp)(const CvpLaunch& L, cudaStream_t stream) {
     if (const char* e = std::getenv("CVPB_NO_TILE"))
         if (e[0] == '1') p.tile_cap = 0;
     p.err = L.err;
+    p.tg = L.targets;
 
     // view chunks whose cut table fits the scratch block
     const int ncols = sc.n1 * sc.n2;
@@ -1288,7 +1299,7 @@ cudaError_t CVP_PUB(launch_cvp)(const CvpLaunch& L, cudaStream_t stream) {
         p.atomic_out = groups > 1 ? 1 : 0;
         // zero-copy float64 output on the last chunk (atomic view groups: convert after)
         p.vol_out64 = (last && groups == 1) ? L.vol_out64 : nullptr;
-        if (!L.forward && groups > 1 && !p.accumulate) {
+        if (!L.forward && groups > 1 && !p.accumulate && L.targets.n == 0) {
             e = cudaMemsetAsync(L.vol_out, 0, sizeof(float) * nvox, stream);
             if (e != cudaSuccess) return e;
         }
@@ -1297,7 +1308,7 @@ cudaError_t CVP_PUB(launch_cvp)(const CvpLaunch& L, cudaStream_t stream) {
         e = L.forward ? launch_opts<true, true>(p, grid, dyn, L.tall_voxels, stream)
                       : launch_opts<true, false>(p, grid, dyn, L.tall_voxels, stream);
         if (e != cudaSuccess) return e;
-        if (!L.forward && last && L.vol_out64 && !p.vol_out64) {
+        if (!L.forward && last && L.vol_out64 && !p.vol_out64 && L.targets.n == 0) {
             e = launch_f32_to_f64(L.vol_out, L.vol_out64, nvox, stream);
             if (e != cudaSuccess) return e;
         }

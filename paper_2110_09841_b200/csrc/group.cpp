@@ -12,10 +12,16 @@
 //   forward   slab upload (H2D, float64 -> float32)  | barrier |
 //             all-gather of the other slabs (peer copies over NVLink), then
 //             the member's views -> its part of the host stack
-//   backward  the member's part of the stack -> a full partial volume | barrier |
-//             reduce-scatter: launch_reduce_slab64 reads the member's slab
-//             out of every member's partial over peer memory, sums the members
-//             in a fixed order, writes float64 -> its slab of the host volume
+//   backward  fused (CVP, default): slabs zeroed | barrier | every member's
+//             bricks add their voxels straight into the owning member's slab
+//             over peer memory (cvpb_backproject_cvp_scatter: the
+//             reduce-scatter overlaps the bricks still computing, no partial
+//             volume exists) | barrier | slab -> float64 -> host;
+//             two-pass (deterministic, TT / Siddon, no peer atomics): the
+//             member's part of the stack -> a full partial volume | barrier |
+//             launch_reduce_slab64 reads the member's slab out of every
+//             member's partial over peer memory, sums the members in a fixed
+//             order, writes float64 -> its slab of the host volume
 //   cgls      the reference's recurrence (solver.cpp:55-106) with x, p, s
 //             held as slabs, r, q as view shards, dots summed over members in
 //             a fixed order; p is all-gathered before every forward.
@@ -136,6 +142,7 @@ struct cvpb_group {
         cvpb_context* ctx = nullptr;
         cudaStream_t st = nullptr;
         cudaEvent_t ev_ready = nullptr;  // this member's slab / partial is ready for its peers
+        cudaEvent_t ev_done = nullptr;   // fused backward: this member's scatter is complete
         cudaEvent_t ev0 = nullptr, ev1 = nullptr;
         int v0 = 0, nv = 0;     // view shard
         size_t s0 = 0, ns = 0;  // volume slab [elements]
@@ -150,6 +157,7 @@ struct cvpb_group {
     };
     std::vector<Member> m;
     bool direct_peer = true;  // every member can load every other member's memory
+    bool peer_atomics = true;  // ... and add to it with native atomics (fused reduce-scatter)
     bool has_geometry = false;
     cvpb_volume_geometry vol{};
     cvpb_detector_geometry det{};
@@ -278,6 +286,46 @@ int reduce_slab(cvpb_group* g, int i, float* out32, double* out64) {
     return CVPB_OK;
 }
 
+// Backward with the reduce-scatter fused in: every member's bricks add their
+// voxels straight into the member slab that owns their planes (`slab32` of
+// each member, float32, peer memory; cvpb_backproject_cvp_scatter). CVP only,
+// not in deterministic mode (atomic order), and only with peer atomics
+// between every pair of members; CVPB_GROUP_FUSED=0 forces the two-pass path
+// (full partial volumes + fixed-order peer-load reduction).
+bool fused_backward(const cvpb_group* g, const Op& op) {
+    if (op.kind != 0 || op.exec.deterministic || !g->direct_peer || !g->peer_atomics) return false;
+    const char* e = std::getenv("CVPB_GROUP_FUSED");
+    return !(e && e[0] == '0');
+}
+
+// slab_of(h) = member h's float32 slab buffer. Zero own slab, meet, scatter
+// this member's views into every slab, meet again: on return (stream order)
+// the member's slab holds the sum over all members.
+template <class SlabOf>
+int scatter_backward(cvpb_group* g, int i, Barrier& bar, const Op& op, const float* proj, SlabOf&& slab_of) {
+    auto& mb = g->m[i];
+    const int n = int(g->m.size());
+    if (mb.ns) G_CUDA(cudaMemsetAsync(slab_of(i), 0, sizeof(float) * mb.ns, mb.st));
+    G_CUDA(cudaEventRecord(mb.ev_ready, mb.st));
+    G_SYNC(bar);  // every member's zeroing is recorded
+    for (int h = 0; h < n; ++h) G_CUDA(cudaStreamWaitEvent(mb.st, g->m[h].ev_ready, 0));
+    if (mb.nv) {
+        cvpb_slab_targets tg{};
+        tg.n = n;
+        const size_t plane = size_t(g->vol.counts[0]) * g->vol.counts[1];
+        for (int h = 0; h < n; ++h) {
+            tg.plane_begin[h] = int(g->m[h].s0 / plane);
+            tg.slab[h] = slab_of(h);
+        }
+        tg.plane_begin[n] = g->vol.counts[2];
+        G_TRY(cvpb_backproject_cvp_scatter(mb.ctx, &op.cvp, &op.exec, proj, mb.v0, mb.nv, &tg, mb.st));
+    }
+    G_CUDA(cudaEventRecord(mb.ev_done, mb.st));
+    G_SYNC(bar);  // every member's scatter is recorded
+    for (int h = 0; h < n; ++h) G_CUDA(cudaStreamWaitEvent(mb.st, g->m[h].ev_done, 0));
+    return CVPB_OK;
+}
+
 // compensated float64 dot of two float32 device vectors, synchronous
 int dot(cvpb_group::Member& mb, const float* a, const float* b, size_t n, double* out) {
     const int np = cvpb::dot_partials_count();
@@ -296,13 +344,14 @@ double sum_published(const cvpb_group* g) {
     return s;
 }
 
-enum { kNeedVol = 1, kNeedPart = 2, kNeedCgls = 4 };
+enum { kNeedVol = 1, kNeedPart = 2, kNeedCgls = 4, kFusedBwd = 8 };
 
 int ensure_buffers(cvpb_group* g, int i, int need) {
     auto& mb = g->m[i];
     const size_t shard = g->npx * size_t(mb.nv);
     if (need & (kNeedVol | kNeedCgls)) G_CUDA(mb.vol.reserve(g->nvox));
-    if (need & (kNeedPart | kNeedCgls)) G_CUDA(mb.part.reserve(g->nvox));
+    // (the fused backward materializes no partial volume)
+    if ((need & kNeedPart) || ((need & kNeedCgls) && !(need & kFusedBwd))) G_CUDA(mb.part.reserve(g->nvox));
     G_CUDA(mb.proj.reserve(shard));
     G_CUDA(mb.stage.reserve(std::max(shard, mb.ns)));
     G_CUDA(mb.partials.reserve(cvpb::dot_partials_count()));
@@ -353,6 +402,22 @@ int forward_host(cvpb_group* g, const Op& op, const double* volume, double* proj
 
 int backward_host(cvpb_group* g, const Op& op, const double* proj, double* volume, double* view_seconds) {
     std::vector<double> secs(g->m.size(), 0.0);
+    if (fused_backward(g, op)) {
+        // no partial volumes: the members' bricks add into the owners' slabs
+        G_TRY(run_members(g, [&](int i, Barrier& bar) -> int {
+            auto& mb = g->m[i];
+            G_TRY(ensure_buffers(g, i, 0));
+            G_CUDA(mb.ss.reserve(mb.ns));
+            const auto t0 = std::chrono::steady_clock::now();
+            G_TRY(upload(mb, proj + g->npx * size_t(mb.v0), mb.proj.p, g->npx * size_t(mb.nv)));
+            G_TRY(scatter_backward(g, i, bar, op, mb.proj.p, [&](int h) { return g->m[h].ss.p; }));
+            G_TRY(download(mb, mb.ss.p, volume + mb.s0, mb.ns));
+            G_CUDA(cudaStreamSynchronize(mb.st));
+            secs[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            return CVPB_OK;
+        }));
+        return fill_view_seconds(g, op, view_seconds, secs);
+    }
     G_TRY(run_members(g, [&](int i, Barrier& bar) -> int {
         auto& mb = g->m[i];
         G_TRY(ensure_buffers(g, i, kNeedPart));
@@ -378,7 +443,8 @@ int cgls_host(cvpb_group* g, const Op& op, const double* b, double* x, int itera
     int err_code = CVPB_OK;
     G_TRY(run_members(g, [&](int i, Barrier& bar) -> int {
         auto& mb = g->m[i];
-        G_TRY(ensure_buffers(g, i, kNeedCgls));
+        const bool fused = fused_backward(g, op);
+        G_TRY(ensure_buffers(g, i, kNeedCgls | (fused ? kFusedBwd : 0)));
         const size_t shard = g->npx * size_t(mb.nv);
         float* r = mb.proj.p;
         float* p_slab = mb.vol.p + mb.s0;
@@ -391,6 +457,7 @@ int cgls_host(cvpb_group* g, const Op& op, const double* b, double* x, int itera
             return CVPB_OK;
         };
         auto adjoint_into_s = [&]() -> int {  // s slab = (A^T r) slab
+            if (fused) return scatter_backward(g, i, bar, op, r, [&](int h) { return g->m[h].ss.p; });
             G_TRY(op_backward(op, mb, g->nvox, r, mb.part.p));
             G_CUDA(cudaEventRecord(mb.ev_ready, mb.st));
             G_SYNC(bar);
@@ -474,6 +541,7 @@ void release_member(cvpb_group::Member& mb) {
     mb.partials.release();
     mb.flag.release();
     if (mb.ev_ready) cudaEventDestroy(mb.ev_ready);
+    if (mb.ev_done) cudaEventDestroy(mb.ev_done);
     if (mb.ev0) cudaEventDestroy(mb.ev0);
     if (mb.ev1) cudaEventDestroy(mb.ev1);
     if (mb.st) cudaStreamDestroy(mb.st);
@@ -511,6 +579,7 @@ int cvpb_group_create(const int* devices, int n_devices, cvpb_group** out) {
             cudaSetDevice(mb.device);
             if (cudaStreamCreateWithFlags(&mb.st, cudaStreamNonBlocking) != cudaSuccess ||
                 cudaEventCreateWithFlags(&mb.ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&mb.ev_done, cudaEventDisableTiming) != cudaSuccess ||
                 cudaEventCreate(&mb.ev0) != cudaSuccess || cudaEventCreate(&mb.ev1) != cudaSuccess)
                 rc = fail(CVPB_CUDA_ERROR, "member stream / event creation failed");
         }
@@ -524,11 +593,17 @@ int cvpb_group_create(const int* devices, int n_devices, cvpb_group** out) {
     for (auto& a : g->m)
         for (auto& b : g->m) {
             if (a.device == b.device) continue;
-            int can = 0;
+            int can = 0, atom = 0;
             cudaDeviceCanAccessPeer(&can, a.device, b.device);
             if (!can) {
                 g->direct_peer = false;
                 continue;
+            }
+            if (cudaDeviceGetP2PAttribute(&atom, cudaDevP2PAttrNativeAtomicSupported, a.device, b.device) !=
+                    cudaSuccess ||
+                !atom) {
+                cudaGetLastError();
+                g->peer_atomics = false;
             }
             cudaSetDevice(a.device);
             const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);

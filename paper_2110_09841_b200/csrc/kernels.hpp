@@ -40,6 +40,9 @@ struct CvpLaunch {
     double* det_g = nullptr;
     unsigned int* det_maxbits = nullptr;
     double det_factor = 0.0;  // voxel count * voxel volume / r_min^2 (bound per unit |mu|)
+    // backward: n > 0 adds each brick's result into the owning slab target
+    // (float atomics, possibly peer memory) instead of writing vol_out
+    SlabTargets targets{};
     int* err;                 // device error flag
 };
 

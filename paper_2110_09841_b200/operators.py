@@ -205,6 +205,31 @@ class DeviceScene:
                                              int(bool(accumulate)), _stream(stream)))
         return out
 
+    def backproject_cvp_scatter(self, proj, slabs, plane_begin, opts: CvpOptions = None,
+                                exec: ExecPolicy = None, view_begin=0, view_count=None, stream=None):
+        """Backprojection fused with a reduce-scatter: planes
+        [plane_begin[t], plane_begin[t+1]) are added (float atomics) into the
+        float32 CUDA tensor slabs[t] — on this or another GPU with peer
+        access — as each brick finishes (cvpb_backproject_cvp_scatter)."""
+        opts = opts or CvpOptions()
+        exec = exec or ExecPolicy()
+        vb, vc = self._range(view_begin, view_count)
+        n = len(slabs)
+        if not 1 <= n <= 16 or len(plane_begin) != n + 1:
+            raise InvalidArgument("slab targets: 1 to 16 slabs and n + 1 plane boundaries")
+        plane = self.vol_geom.counts[0] * self.vol_geom.counts[1]
+        tg = N.cvpb_slab_targets()
+        tg.n = n
+        for t in range(n + 1):
+            tg.plane_begin[t] = int(plane_begin[t])
+        for t, sl in enumerate(slabs):
+            cnt = (int(plane_begin[t + 1]) - int(plane_begin[t])) * plane
+            tg.slab[t] = _ptr(sl, cnt).value if cnt > 0 else None
+        N.check(N.lib().cvpb_backproject_cvp_scatter(self._h, C.byref(opts._c()), C.byref(exec._c()),
+                                                     self._stk(proj, vc), vb, vc, C.byref(tg),
+                                                     _stream(stream)))
+        return slabs
+
     def project_cvp_host(self, vol64: np.ndarray, out64: np.ndarray = None,
                          opts: CvpOptions = None, exec: ExecPolicy = None, view_seconds=None):
         """Reference-facing path: float64 host buffers, copies inside."""

@@ -11,9 +11,11 @@ Bars:
   as the single-context path -> equal to the one-context host path within
   float32 atomic reassociation (1e-6), and to the reference Double within the
   north-star bar (rel-L2 1e-5, max 1e-4);
-* backward: partials summed in a fixed member order in float64 -> within
-  float32 reassociation of the one-context result, and within the bar of the
-  reference;
+* backward: fused (default for CVP): every member's bricks add into the
+  owning member's slab with float atomics over peer memory; two-pass
+  (deterministic / CVPB_GROUP_FUSED=0): partials summed in a fixed member
+  order in float64 -> both within float32 reassociation of the one-context
+  result, and within the bar of the reference;
 * CGLS: the residual history of the group equals the single-device
   device-resident CGLS (rtol 1e-5) and the reference's cgls (rtol 1e-5).
 """
@@ -173,3 +175,59 @@ def test_reference_unit_tests_through_a_two_member_group(unit):
     assert cases, out.stdout[-2000:] + out.stderr[-2000:]
     bad = [(n, int(f)) for n, c, f in cases if int(f) and n not in EXPECTED_PRECISION_MISSES]
     assert not bad, out.stdout[-4000:]
+
+
+def test_backproject_scatter_matches_the_device_backprojection():
+    """cvpb_backproject_cvp_scatter on one context: planes split unevenly over
+    four targets (one empty) equal the plain device backprojection's planes,
+    targets holding values are added to, and bad targets / deterministic mode
+    are refused."""
+    import torch
+    import paper_2110_09841_b200 as cb
+    from paper_2110_09841_b200._native import InvalidArgument
+    geom, det, views, _ = make_case(*CASE)
+    sc = cb.DeviceScene(geom, det, views)
+    _, b = _data(geom, det, len(views))
+    proj = torch.from_numpy(b.astype(np.float32)).reshape(len(views), det.rows, det.cols).cuda()
+    n1, n2, n3 = geom.counts
+    full = sc.backproject_cvp(proj)
+    bounds = [0, 5, 5, 21, n3]
+    slabs = [torch.zeros((bounds[t + 1] - bounds[t], n2, n1), device="cuda") for t in range(4)]
+    sc.backproject_cvp_scatter(proj, slabs, bounds)
+    got = torch.cat(slabs, 0)
+    torch.cuda.synchronize()
+    assert rel_l2(got.double().cpu().numpy(), full.double().cpu().numpy()) < 1e-6
+    # adds into what the targets hold; a view sub-range scatters only its views
+    sc.backproject_cvp_scatter(proj[3:8], slabs, bounds, view_begin=3, view_count=5)
+    part = sc.backproject_cvp(proj[3:8], view_begin=3, view_count=5)
+    torch.cuda.synchronize()
+    assert rel_l2((torch.cat(slabs, 0) - full).double().cpu().numpy(), part.double().cpu().numpy()) < 1e-5
+    with pytest.raises(InvalidArgument):
+        sc.backproject_cvp_scatter(proj, slabs, [0, 5, 5, 21, n3 - 1])
+    with pytest.raises(InvalidArgument):
+        sc.backproject_cvp_scatter(proj, slabs, [0, 5, 4, 21, n3])
+    with pytest.raises(InvalidArgument):
+        sc.backproject_cvp_scatter(proj, slabs, bounds, exec=cb.ExecPolicy(deterministic=True))
+    sc.close()
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0]])
+def test_group_fused_backward_matches_two_pass(devices, monkeypatch, reference):
+    """The fused reduce-scatter (atomics into the owners' slabs) against the
+    two-pass path (full partials + fixed-order peer-load reduction) and the
+    reference; CGLS through the fused adjoint against the two-pass one."""
+    import paper_2110_09841_b200 as cb
+    geom, det, views, sc = make_case(*CASE)
+    x, b = _data(geom, det, len(views))
+    grp = cb.GroupScene(geom, det, views, devices=devices)
+    fused = grp.backproject_cvp_host(b)
+    x_fused, h_fused = grp.cgls_host(b, 4)
+    monkeypatch.setenv("CVPB_GROUP_FUSED", "0")
+    two = grp.backproject_cvp_host(b)
+    x_two, h_two = grp.cgls_host(b, 4)
+    assert rel_l2(fused, two) < 1e-6 and max_rel(fused, two) < 1e-5
+    ref = reference.backproject_cvp(sc, b, (1, 1, 0, 1), threads=THREADS)
+    assert rel_l2(fused, ref) <= 1e-5 and max_rel(fused, ref) <= 1e-4
+    np.testing.assert_allclose(h_fused, h_two, rtol=1e-5)
+    assert rel_l2(x_fused, x_two) < 1e-5
+    grp.close()
