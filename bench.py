@@ -308,6 +308,14 @@ def run_native(args):
     bp = scene.new_volume()
     slab = torch.empty(nvox // world if world > 1 else 1, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
+    # N > 1: the backprojection fused with its reduce-scatter — every rank's
+    # bricks add into the owning rank's z-slab over CUDA IPC / NVLink
+    # (parallel.PeerSlabs); NCCL reduce_scatter_tensor when that is off
+    peers = None
+    if world > 1:
+        from paper_2110_09841_b200 import parallel as par
+        if par.fused_reduce_scatter_ok(scene, "cvp"):
+            peers = par.PeerSlabs(scene)
 
     def step(ev=None):
         if ev:
@@ -315,10 +323,18 @@ def run_native(args):
         scene.project_cvp(x, p, opts, view_begin=v0, view_count=v1 - v0)
         if ev:
             ev[1].record(stream)
-        scene.backproject_cvp(b, bp, opts, view_begin=v0, view_count=v1 - v0)
+        if peers is not None:
+            peers.own.zero_()
+            peers._barrier()  # every slab zeroed before anyone adds
+            scene.backproject_cvp_scatter(b, peers.ptrs, peers.bounds, opts, view_begin=v0,
+                                          view_count=v1 - v0)
+        else:
+            scene.backproject_cvp(b, bp, opts, view_begin=v0, view_count=v1 - v0)
         if ev:
             ev[2].record(stream)
-        if world > 1:
+        if peers is not None:
+            peers._barrier()  # every rank's adds have landed in this rank's slab
+        elif world > 1:
             dist.reduce_scatter_tensor(slab, bp.view(-1))
         if ev:
             ev[3].record(stream)
@@ -544,6 +560,7 @@ def run_native(args):
                "data": "synthetic",
                "config": config_dict(args, world),
                "p_ms": pm, "bp_ms": bm, "cgls": cgls, "reduce_scatter_ms": rm if world > 1 else 0.0,
+               "exchange": ("none" if world == 1 else "fused backprojection + reduce-scatter (CUDA IPC slabs, NVLink atomics)" if peers is not None else "NCCL reduce_scatter_tensor"),
                "p_gvps": work / world / (pm * 1e-3), "bp_gvps": work / world / (bm * 1e-3),
                # per step: cvp_brick_kernel<FWD> + apply_scale_kernel, cvp_brick_kernel<BWD>
                # (profiles/launches_r0*.csv); the cut table was built (and the brick

@@ -107,6 +107,13 @@ typedef struct cvpb_context cvpb_context;
 /* ---- library / context -------------------------------------------------- */
 int cvpb_abi_version(void);
 const char* cvpb_last_error(void);
+/* The device-buffer calls are asynchronous: geometry degeneracies a kernel
+ * detects (voxel base reaching the source plane -> CVPB_RUNTIME_ERROR, a
+ * degenerate cut polygon -> CVPB_DOMAIN_ERROR, the reference's exceptions)
+ * are raised as device flags. cvpb_sync waits for `stream` (NULL: the
+ * context's own stream) and reports and clears the flags raised since the
+ * last report; the host-buffer calls do this themselves. */
+int cvpb_sync(cvpb_context* ctx, void* stream);
 int cvpb_device_count(int* out);
 int cvpb_context_create(int device, cvpb_context** out);
 void cvpb_context_destroy(cvpb_context* ctx);
@@ -181,6 +188,16 @@ typedef struct cvpb_slab_targets {
 int cvpb_backproject_cvp_scatter(cvpb_context* ctx, const cvpb_cvp_options* opts,
                                  const cvpb_exec_policy* exec, const float* d_proj, int view_begin,
                                  int view_count, const cvpb_slab_targets* targets, void* stream);
+
+/* Device buffers shared between processes (CUDA IPC), so one process per GPU
+ * can run cvpb_backproject_cvp_scatter into the other ranks' slabs: alloc
+ * exports a 64-byte handle of a fresh buffer on the context's device; open
+ * maps another process's buffer (peer access enabled on demand); close
+ * unmaps it; free releases an allocated buffer. */
+int cvpb_ipc_alloc(cvpb_context* ctx, size_t bytes, void** d_ptr, unsigned char handle[64]);
+int cvpb_ipc_open(cvpb_context* ctx, const unsigned char handle[64], void** d_ptr);
+int cvpb_ipc_close(cvpb_context* ctx, void* d_ptr);
+int cvpb_ipc_free(cvpb_context* ctx, void* d_ptr);
 
 /* ---- CVP — reference-facing host path (float64 host buffers, H2D/D2H inside) */
 int cvpb_project_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,

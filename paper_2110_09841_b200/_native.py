@@ -83,6 +83,11 @@ SIGNATURES = {
                                         _vp, _vp]),
     "cvpb_backproject_cvp_host": (C.c_int, [_vp, _P(cvpb_cvp_options), _P(cvpb_exec_policy), _vp,
                                             _vp, _vp]),
+    "cvpb_sync": (C.c_int, [_vp, _vp]),
+    "cvpb_ipc_alloc": (C.c_int, [_vp, C.c_size_t, _P(C.c_void_p), _vp]),
+    "cvpb_ipc_open": (C.c_int, [_vp, _vp, _P(C.c_void_p)]),
+    "cvpb_ipc_close": (C.c_int, [_vp, _vp]),
+    "cvpb_ipc_free": (C.c_int, [_vp, _vp]),
     "cvpb_backproject_cvp_scatter": (C.c_int, [_vp, _P(cvpb_cvp_options), _P(cvpb_exec_policy), _vp,
                                                C.c_int, C.c_int, _P(cvpb_slab_targets), _vp]),
     "cvpb_cvp_view_weights": (C.c_int, [_vp, _P(cvpb_cvp_options), C.c_int, C.c_int, _dp]),

@@ -1004,6 +1004,51 @@ int fill_view_seconds(cvpb_context* ctx, const cvpb_cvp_options* opts, int nview
 }
 }  // namespace
 
+int cvpb_ipc_alloc(cvpb_context* ctx, size_t bytes, void** d_ptr, unsigned char handle[64]) {
+    CVPB_TRY(check_ctx(ctx, false));
+    if (!d_ptr || !handle) return fail(CVPB_INVALID_ARGUMENT, "null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handle size");
+    void* p = nullptr;
+    CVPB_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 1)));
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        CVPB_CUDA(e);
+    }
+    std::memcpy(handle, &h, 64);
+    *d_ptr = p;
+    return CVPB_OK;
+}
+
+int cvpb_ipc_open(cvpb_context* ctx, const unsigned char handle[64], void** d_ptr) {
+    CVPB_TRY(check_ctx(ctx, false));
+    if (!d_ptr || !handle) return fail(CVPB_INVALID_ARGUMENT, "null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    CVPB_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return CVPB_OK;
+}
+
+int cvpb_ipc_close(cvpb_context* ctx, void* d_ptr) {
+    CVPB_TRY(check_ctx(ctx, false));
+    if (d_ptr) CVPB_CUDA(cudaIpcCloseMemHandle(d_ptr));
+    return CVPB_OK;
+}
+
+int cvpb_ipc_free(cvpb_context* ctx, void* d_ptr) {
+    CVPB_TRY(check_ctx(ctx, false));
+    if (d_ptr) CVPB_CUDA(cudaFree(d_ptr));
+    return CVPB_OK;
+}
+
+int cvpb_sync(cvpb_context* ctx, void* stream) {
+    CVPB_TRY(check_ctx(ctx, false));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    CVPB_CUDA(cudaStreamSynchronize(st));
+    return device_error(ctx, st);
+}
+
 int cvpb_backproject_cvp_scatter(cvpb_context* ctx, const cvpb_cvp_options* opts,
                                  const cvpb_exec_policy* exec, const float* d_proj, int view_begin,
                                  int view_count, const cvpb_slab_targets* targets, void* stream) {

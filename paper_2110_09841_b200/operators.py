@@ -154,6 +154,11 @@ class DeviceScene:
     def n_views(self):
         return len(self.views)
 
+    def synchronize(self, stream=None):
+        """Wait for the stream and raise the reference's exception for any
+        geometry degeneracy an asynchronous device call flagged (cvpb_sync)."""
+        N.check(N.lib().cvpb_sync(self._h, _stream(stream)))
+
     def _torch_device(self):
         import torch
         return torch.device("cuda", self.device)
@@ -208,9 +213,10 @@ class DeviceScene:
     def backproject_cvp_scatter(self, proj, slabs, plane_begin, opts: CvpOptions = None,
                                 exec: ExecPolicy = None, view_begin=0, view_count=None, stream=None):
         """Backprojection fused with a reduce-scatter: planes
-        [plane_begin[t], plane_begin[t+1]) are added (float atomics) into the
-        float32 CUDA tensor slabs[t] — on this or another GPU with peer
-        access — as each brick finishes (cvpb_backproject_cvp_scatter)."""
+        [plane_begin[t], plane_begin[t+1]) are added (float atomics) into
+        slabs[t] — a float32 CUDA tensor or a raw device address, on this or
+        another GPU with peer access — as each brick finishes
+        (cvpb_backproject_cvp_scatter)."""
         opts = opts or CvpOptions()
         exec = exec or ExecPolicy()
         vb, vc = self._range(view_begin, view_count)
@@ -224,7 +230,10 @@ class DeviceScene:
             tg.plane_begin[t] = int(plane_begin[t])
         for t, sl in enumerate(slabs):
             cnt = (int(plane_begin[t + 1]) - int(plane_begin[t])) * plane
-            tg.slab[t] = _ptr(sl, cnt).value if cnt > 0 else None
+            if isinstance(sl, int):  # a raw device address (e.g. another process's buffer, CUDA IPC)
+                tg.slab[t] = sl
+            else:
+                tg.slab[t] = _ptr(sl, cnt).value if cnt > 0 else None
         N.check(N.lib().cvpb_backproject_cvp_scatter(self._h, C.byref(opts._c()), C.byref(exec._c()),
                                                      self._stk(proj, vc), vb, vc, C.byref(tg),
                                                      _stream(stream)))

@@ -13,6 +13,16 @@ Views are sharded contiguously across ranks:
   all-gathers p before each forward projection and all-reduces the float64
   dot-product scalars (solver.cpp:55-106 recurrence).
 
+For CVP the backprojection and its reduce-scatter are one kernel
+(:class:`PeerSlabs`): every rank's z-slab buffer is mapped into every other
+rank's process with CUDA IPC, and each rank's bricks add their voxels
+straight into the owning rank's slab over NVLink as they finish
+(cvpb_backproject_cvp_scatter) — no partial volume, no NCCL reduce-scatter;
+two 1-element NCCL all-reduces order the ranks' streams (slabs zeroed before
+anyone adds, all adds done before anyone reads). NCCL's reduce_scatter_tensor
+remains the path for TT / Siddon, deterministic mode, and volumes whose plane
+count the world size does not divide (``CVPB_FUSED_RS=0`` forces it).
+
 The per-rank compute is injected (``forward_local`` / ``adjoint_local`` and a
 ``vec`` object), so the same orchestration runs over libcvpb200 on GPUs and
 over a CPU stand-in in the gloo tests.
@@ -50,9 +60,12 @@ class DistributedOperator:
     """
 
     def __init__(self, forward_local: Callable, adjoint_local: Callable, n_vox: int,
-                 local_stack_shape, device, group=None):
+                 local_stack_shape, device, group=None, adjoint_scatter: Callable = None):
         self.forward_local = forward_local
         self.adjoint_local = adjoint_local
+        # adjoint_scatter(b_local) -> this rank's summed slab (fused
+        # backprojection + reduce-scatter, PeerSlabs); None: partial + NCCL
+        self.adjoint_scatter = adjoint_scatter
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -115,10 +128,105 @@ class DistributedOperator:
                     partial: torch.Tensor = None):
         if out_slab is None:
             out_slab = self.new_slab()
+        if self.adjoint_scatter is not None:
+            own = self.adjoint_scatter(b_local)
+            out_slab[: own.numel()].copy_(own)
+            return out_slab
         if partial is None:
             partial = torch.zeros(self.n_vox, dtype=torch.float32, device=self.device)
         self.adjoint_local(b_local, partial)
         return self.reduce_scatter(partial, out_slab)
+
+
+class _CudaBuffer:
+    """__cuda_array_interface__ view of a raw float32 device buffer (so torch
+    can wrap library-allocated IPC memory without a copy)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f4", "data": (int(ptr), False),
+                                         "version": 2, "strides": None}
+
+
+class PeerSlabs:
+    """The z-slabs of all ranks, each mapped into every rank's process (CUDA
+    IPC), for the fused backprojection + reduce-scatter of CVP.
+
+    Rank r owns planes [r * N3 / world, (r + 1) * N3 / world) (N3 divisible by
+    the world size, so the slabs are the same contiguous element ranges the
+    NCCL path uses). :meth:`backproject` returns this rank's slab summed over
+    all ranks' views."""
+
+    def __init__(self, scene, group=None):
+        import ctypes as C
+        from . import _native as N
+        self.scene, self.group = scene, group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        n1, n2, n3 = scene.vol_geom.counts
+        if n3 % self.world:
+            raise InvalidArgument("PeerSlabs needs a plane count divisible by the world size")
+        planes = n3 // self.world
+        self.elems = planes * n1 * n2
+        self.bounds = [r * planes for r in range(self.world + 1)]
+        L = N.lib()
+        own = C.c_void_p()
+        handle = (C.c_char * 64)()
+        N.check(L.cvpb_ipc_alloc(scene._h, self.elems * 4, C.byref(own), C.cast(handle, C.c_void_p)))
+        self._own_ptr = own.value
+        handles = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(handles, bytes(handle), group=group)
+        self._opened = []
+        self.ptrs = []
+        for r in range(self.world):
+            if r == self.rank:
+                self.ptrs.append(self._own_ptr)
+                continue
+            hb = (C.c_char * 64).from_buffer_copy(handles[r])
+            p = C.c_void_p()
+            N.check(L.cvpb_ipc_open(scene._h, C.cast(hb, C.c_void_p), C.byref(p)))
+            self._opened.append(p.value)
+            self.ptrs.append(p.value)
+        self.own = torch.as_tensor(_CudaBuffer(self._own_ptr, self.elems),
+                                   device=torch.device("cuda", scene.device))
+        # device-side barrier: a 1-element NCCL all-reduce completes on every
+        # rank's stream only after all ranks' earlier stream work (gloo, in
+        # tests: synchronize + host barrier)
+        self._nccl = dist.is_initialized() and dist.get_backend(group) == "nccl"
+        self._one = torch.zeros(1, dtype=torch.float32, device=self.own.device)
+
+    def _barrier(self):
+        if self.world == 1:
+            return
+        if self._nccl:
+            dist.all_reduce(self._one, group=self.group)
+        else:
+            torch.cuda.synchronize(self.own.device)
+            dist.barrier(group=self.group)
+
+    def backproject(self, b_local, opts, view_begin, view_count, stream=None):
+        """This rank's views backprojected into every rank's slab; returns the
+        own slab (flat float32) once every rank's adds have landed."""
+        self.own.zero_()
+        self._barrier()  # every slab is zeroed before anyone adds
+        if view_count > 0:
+            self.scene.backproject_cvp_scatter(b_local, self.ptrs, self.bounds, opts,
+                                               view_begin=view_begin, view_count=view_count,
+                                               stream=stream)
+        self._barrier()  # every rank's adds are complete
+        return self.own
+
+    def close(self):
+        from . import _native as N
+        L = N.lib()
+        torch.cuda.synchronize(self.own.device)
+        for p in self._opened:
+            L.cvpb_ipc_close(self.scene._h, p)
+        self._opened = []
+        if self._own_ptr:
+            self.own = None
+            L.cvpb_ipc_free(self.scene._h, self._own_ptr)
+            self._own_ptr = None
 
 
 class TorchVec:
@@ -202,9 +310,20 @@ def distributed_cgls(op: DistributedOperator, b_local: torch.Tensor, iterations:
     return DistributedCglsResult(x, res)
 
 
+def fused_reduce_scatter_ok(scene, projector: str = "cvp", exec=None, group=None) -> bool:
+    """Whether the CVP backprojection can run fused with the reduce-scatter
+    (PeerSlabs): CVP, not deterministic, several ranks, N3 divisible by the
+    world size, not disabled by CVPB_FUSED_RS=0."""
+    import os
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    return (projector == "cvp" and world > 1 and not (exec is not None and exec.deterministic)
+            and scene.vol_geom.counts[2] % world == 0 and os.environ.get("CVPB_FUSED_RS", "1") != "0")
+
+
 def scene_operator(scene, opts=None, projector: str = "cvp", k_per_edge: int = 1,
                    group=None) -> DistributedOperator:
-    """DistributedOperator over a DeviceScene: this rank's view shard."""
+    """DistributedOperator over a DeviceScene: this rank's view shard (CVP:
+    the backprojection fused with the reduce-scatter when possible)."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     vb, vc = view_shard(scene.n_views, world, rank)
@@ -228,6 +347,13 @@ def scene_operator(scene, opts=None, projector: str = "cvp", k_per_edge: int = 1
         else:
             scene.backproject_tt(b_local, out, view_begin=vb, view_count=vc)
 
+    scatter = None
+    if fused_reduce_scatter_ok(scene, projector, group=group):
+        peers = PeerSlabs(scene, group)
+
+        def scatter(b_local):
+            return peers.backproject(b_local, opts, vb, vc)
+        scatter.peers = peers
     return DistributedOperator(fwd, adj, scene.vol_geom.voxel_count(),
                                (vc, scene.det.rows, scene.det.cols),
-                               torch.device("cuda", scene.device), group)
+                               torch.device("cuda", scene.device), group, adjoint_scatter=scatter)

@@ -128,3 +128,18 @@ def test_view_seconds_attribute_the_call_time_by_view_work():
     w2 = sc.cvp_view_weights(opts, view_begin=2, view_count=3)
     np.testing.assert_allclose(w2, w[2:5] / w[2:5].sum(), rtol=1e-12)
     sc.close()
+
+
+def test_sync_reports_no_error_after_clean_device_calls():
+    """cvpb_sync: device-path calls are asynchronous; a clean sequence
+    reports nothing (and the context's own stream is accepted)."""
+    import torch
+    import paper_2110_09841_b200 as cb
+    _, geom, _, _, sc = _scene(nv=8, n=16)
+    x = torch.rand(geom.shape(), device="cuda")
+    p = sc.project_cvp(x)
+    sc.backproject_cvp(p)
+    sc.synchronize()
+    from paper_2110_09841_b200 import _native as N
+    N.check(N.lib().cvpb_sync(sc._h, None))
+    sc.close()
