@@ -315,7 +315,10 @@ def run_native(args):
     if world > 1:
         from paper_2110_09841_b200 import parallel as par
         if par.fused_reduce_scatter_ok(scene, "cvp"):
-            peers = par.PeerSlabs(scene)
+            try:
+                peers = par.PeerSlabs(scene)
+            except RuntimeError:  # (every rank alike) -> NCCL reduce-scatter
+                peers = None
 
     def step(ev=None):
         if ev:

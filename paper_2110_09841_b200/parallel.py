@@ -171,22 +171,42 @@ class PeerSlabs:
         L = N.lib()
         own = C.c_void_p()
         handle = (C.c_char * 64)()
-        N.check(L.cvpb_ipc_alloc(scene._h, self.elems * 4, C.byref(own), C.cast(handle, C.c_void_p)))
-        self._own_ptr = own.value
-        handles = [None] * self.world
-        if self.world > 1:
-            dist.all_gather_object(handles, bytes(handle), group=group)
+        # every step is agreed on by all ranks (a rank that fails alone must
+        # not leave the others waiting in a collective): on any failure every
+        # rank releases what it mapped and raises, and callers fall back to
+        # the NCCL reduce-scatter
+        ok = L.cvpb_ipc_alloc(scene._h, self.elems * 4, C.byref(own), C.cast(handle, C.c_void_p)) == 0
+        self._own_ptr = own.value if ok else None
         self._opened = []
+        msgs = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(msgs, (ok, bytes(handle)), group=group)
+        else:
+            msgs = [(ok, bytes(handle))]
         self.ptrs = []
-        for r in range(self.world):
-            if r == self.rank:
-                self.ptrs.append(self._own_ptr)
-                continue
-            hb = (C.c_char * 64).from_buffer_copy(handles[r])
-            p = C.c_void_p()
-            N.check(L.cvpb_ipc_open(scene._h, C.cast(hb, C.c_void_p), C.byref(p)))
-            self._opened.append(p.value)
-            self.ptrs.append(p.value)
+        if all(m[0] for m in msgs):
+            for r in range(self.world):
+                if r == self.rank:
+                    self.ptrs.append(self._own_ptr)
+                    continue
+                hb = (C.c_char * 64).from_buffer_copy(msgs[r][1])
+                p = C.c_void_p()
+                if L.cvpb_ipc_open(scene._h, C.cast(hb, C.c_void_p), C.byref(p)) != 0:
+                    ok = False
+                    break
+                self._opened.append(p.value)
+                self.ptrs.append(p.value)
+        else:
+            ok = False
+        flags = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(flags, ok, group=group)
+        else:
+            flags = [ok]
+        if not all(flags):
+            self.own = None
+            self._release()
+            raise RuntimeError("CUDA IPC slab mapping failed on at least one rank")
         self.own = torch.as_tensor(_CudaBuffer(self._own_ptr, self.elems),
                                    device=torch.device("cuda", scene.device))
         # device-side barrier: a 1-element NCCL all-reduce completes on every
@@ -216,17 +236,21 @@ class PeerSlabs:
         self._barrier()  # every rank's adds are complete
         return self.own
 
-    def close(self):
+    def _release(self):
         from . import _native as N
         L = N.lib()
-        torch.cuda.synchronize(self.own.device)
         for p in self._opened:
             L.cvpb_ipc_close(self.scene._h, p)
         self._opened = []
         if self._own_ptr:
-            self.own = None
             L.cvpb_ipc_free(self.scene._h, self._own_ptr)
             self._own_ptr = None
+
+    def close(self):
+        if self.own is not None:
+            torch.cuda.synchronize(self.own.device)
+        self.own = None
+        self._release()
 
 
 class TorchVec:
@@ -349,11 +373,14 @@ def scene_operator(scene, opts=None, projector: str = "cvp", k_per_edge: int = 1
 
     scatter = None
     if fused_reduce_scatter_ok(scene, projector, group=group):
-        peers = PeerSlabs(scene, group)
-
-        def scatter(b_local):
-            return peers.backproject(b_local, opts, vb, vc)
-        scatter.peers = peers
+        try:
+            peers = PeerSlabs(scene, group)
+        except RuntimeError:  # (raised on every rank alike) -> NCCL reduce-scatter
+            peers = None
+        if peers is not None:
+            def scatter(b_local):
+                return peers.backproject(b_local, opts, vb, vc)
+            scatter.peers = peers
     return DistributedOperator(fwd, adj, scene.vol_geom.voxel_count(),
                                (vc, scene.det.rows, scene.det.cols),
                                torch.device("cuda", scene.device), group, adjoint_scatter=scatter)
