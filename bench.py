@@ -284,9 +284,18 @@ def run_native(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CVPB_BENCH_SHARE_GPU=1 (code-path check on a one-GPU box, never a
+    # measurement): every rank on cuda:0 over gloo
+    share = os.environ.get("CVPB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    coll_dev = "cpu" if share else "cuda"  # device of the small timing all-reduces
 
     c = CONFIG
     det = cb.DetectorGeometry.make(c["rows"], c["cols"], c["pw"], c["ph"])
@@ -369,7 +378,7 @@ def run_native(args):
     rs_ms = [e[2].elapsed_time(e[3]) for e in evs]
     if world > 1:
         t = torch.tensor([total_ms, statistics.mean(p_ms), statistics.mean(bp_ms),
-                          statistics.mean(rs_ms)], device="cuda")
+                          statistics.mean(rs_ms)], device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, pm, bm, rm = t.tolist()
     else:
@@ -427,7 +436,7 @@ def run_native(args):
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / e2e_steps
         if world > 1:
-            d = torch.tensor([dt], device="cuda")
+            d = torch.tensor([dt], device=coll_dev)
             dist.all_reduce(d, op=dist.ReduceOp.MAX)
             dt = float(d.item())
         e2e = {"value": work / dt, "unit": UNIT,
@@ -484,13 +493,15 @@ def run_native(args):
         run(1)  # warm-up
         ta, _ = run(1)
         tb, r = run(1 + args.cgls_iters)
-        dt = torch.tensor([(tb - ta) / args.cgls_iters], device="cuda")
+        dt = torch.tensor([(tb - ta) / args.cgls_iters], device=coll_dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         cgls = {"ms_per_iter": float(dt.item()) * 1e3, "iterations_timed": args.cgls_iters,
                 "residual_ratio": r.residual_norms[-1] / r.residual_norms[0],
                 "how": f"view-sharded CGLS over {world} ranks on the c3 scene (parallel."
-                       "distributed_cgls: slab-resident x/s/p, NCCL all-gather + reduce-scatter "
-                       "per iteration); ms/iter = (T(1+n) - T(1)) / n, max over ranks"}
+                       "distributed_cgls: slab-resident x/s/p, all-gather of p + "
+                       + ("backprojection fused with the reduce-scatter (CUDA IPC slabs) "
+                          if op.adjoint_scatter is not None else "NCCL reduce-scatter ")
+                       + "per iteration); ms/iter = (T(1+n) - T(1)) / n, max over ranks"}
 
     # ---- roofline of the dominant kernel -----------------------------------
     hbm, peak_src = _peaks()
