@@ -458,7 +458,7 @@ template <int NB, class Emit>
 __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh, float pmh, float dz,
                                                float h, float sh, const bool per_row_r,
                                                float inv_r2_fixed, float wscale, Emit&& emit) {
-    static_assert(NB == 1 || NB == 2, "one or two interior boundaries");
+    static_assert(NB >= 1 && NB <= 3, "one to three interior boundaries");
     constexpr float kMagic = 12582912.f;
     constexpr int kMagicBits = 0x4B400000;
     const float tr = fmaf(fabsf(dz), c.tr_b, c.tr_a);
@@ -501,20 +501,46 @@ __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh
         const float2 rr = make_float2(fast_rcp(fmaxf(s1, 1e-30f)), fast_rcp(fmaxf(s2, 1e-30f)));
         const float2 T = fma2(mul2(num, rr), make_float2(0.25f, 0.25f), make_float2(p1, p2));
         const float2 S = sub2(make_float2(h, T.x), T);
-        float2 I = make_float2(inv_r2_fixed * wscale, inv_r2_fixed * wscale);
-        float i2 = I.x;
-        if (per_row_r) {
-            const float2 Z = fma2(add2(make_float2(h, p1), make_float2(p1, p2)), make_float2(0.5f, 0.5f),
-                                  make_float2(dz, dz));
-            const float z2 = fmaf(0.5f, p2 - h, dz);
-            const float2 Q = fma2(Z, Z, make_float2(c.rho2, c.rho2));
-            I = mul2(make_float2(fast_rcp(Q.x), fast_rcp(Q.y)), make_float2(wscale, wscale));
-            i2 = fast_rcp(fmaf(z2, z2, c.rho2)) * wscale;
+        if constexpr (NB == 2) {
+            float2 I = make_float2(inv_r2_fixed * wscale, inv_r2_fixed * wscale);
+            float i2 = I.x;
+            if (per_row_r) {
+                const float2 Z = fma2(add2(make_float2(h, p1), make_float2(p1, p2)),
+                                      make_float2(0.5f, 0.5f), make_float2(dz, dz));
+                const float z2 = fmaf(0.5f, p2 - h, dz);
+                const float2 Q = fma2(Z, Z, make_float2(c.rho2, c.rho2));
+                I = mul2(make_float2(fast_rcp(Q.x), fast_rcp(Q.y)), make_float2(wscale, wscale));
+                i2 = fast_rcp(fmaf(z2, z2, c.rho2)) * wscale;
+            }
+            const float2 W = mul2(make_float2(fmaxf(S.x, 0.f), fmaxf(S.y, 0.f)), I);
+            emit(m_first, W.x);
+            emit(m_first + 1, W.y);
+            emit(m_first + 2, fmaxf(T.y + h, 0.f) * i2);
+        } else {
+            // third interior boundary (voxels up to ~3 rows tall: configs[1])
+            const float e3 = e1 + 2.f;
+            const float a3 = c.g * (uh - e3);
+            const float p3 = clampf(a3, -h, h);
+            const float t3 = clamp_mean_local(a3, sh * fabsf(pmh - e3), h);
+            const float2 S2 = make_float2(T.y - t3, t3 + h);
+            float2 I = make_float2(inv_r2_fixed * wscale, inv_r2_fixed * wscale), I2 = I;
+            if (per_row_r) {
+                const float2 Z = fma2(add2(make_float2(h, p1), make_float2(p1, p2)),
+                                      make_float2(0.5f, 0.5f), make_float2(dz, dz));
+                const float2 Z2 = fma2(add2(make_float2(p2, p3), make_float2(p3, -h)),
+                                       make_float2(0.5f, 0.5f), make_float2(dz, dz));
+                const float2 Q = fma2(Z, Z, make_float2(c.rho2, c.rho2));
+                const float2 Q2 = fma2(Z2, Z2, make_float2(c.rho2, c.rho2));
+                I = mul2(make_float2(fast_rcp(Q.x), fast_rcp(Q.y)), make_float2(wscale, wscale));
+                I2 = mul2(make_float2(fast_rcp(Q2.x), fast_rcp(Q2.y)), make_float2(wscale, wscale));
+            }
+            const float2 W = mul2(make_float2(fmaxf(S.x, 0.f), fmaxf(S.y, 0.f)), I);
+            const float2 W2 = mul2(make_float2(fmaxf(S2.x, 0.f), fmaxf(S2.y, 0.f)), I2);
+            emit(m_first, W.x);
+            emit(m_first + 1, W.y);
+            emit(m_first + 2, W2.x);
+            emit(m_first + 3, W2.y);
         }
-        const float2 W = mul2(make_float2(fmaxf(S.x, 0.f), fmaxf(S.y, 0.f)), I);
-        emit(m_first, W.x);
-        emit(m_first + 1, W.y);
-        emit(m_first + 2, fmaxf(T.y + h, 0.f) * i2);
     }
 }
 

@@ -154,8 +154,8 @@ struct Smem {
     float mu_abs_max;         // forward: max |mu| over the brick
     int nonfinite;            // forward: the brick holds a NaN / Inf attenuation
     float qscale;             // forward: fixed-point scale of this (brick, view)
-    int walk_mode;            // 0: general row walk; 1 / 2: walk_rows_fast<1 / 2>;
-                              // 3 / 4: the same with rows off the detector dropped
+    int walk_mode;            // 0: general row walk; 1 / 2 / 3: walk_rows_fast<1 / 2 / 3>;
+                              // 5 / 6 / 7: the same with rows off the detector dropped
 };
 
 // 32-bit shared-window addressing for the hot paths: with 80 registers the
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                     const float dzm = fmaxf(fabsf(zlo), fabsf(zhi));
                     const float rdl = 1.f / dl;
                     const float tr = (0.5f * float(sc.a3) + dzm * ddm / dmin) * fb2 * rdl * 1.0001f + 2e-5f;
-                    mode = 2.f * tr < 0.999f ? 1 : 2.f * tr < 1.999f ? 2 : 0;
+                    mode = 2.f * tr < 0.999f ? 1 : 2.f * tr < 1.999f ? 2 : 2.f * tr < 2.999f ? 3 : 0;
                     // a brick whose rows reach past the detector's top or
                     // bottom edge walks the same rows and drops the records
                     // of rows off the detector: a row's share depends only
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                             m0 = r0u;
                             m1 = r1u;
                         } else {
-                            mode += 2;
+                            mode += 4;
                         }
                     }
                 }
@@ -742,8 +742,8 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             auto fast_cut = [&](const CutRec& r, VoxState& v) {
                 // (fast mode: the elevation gate holds for every voxel-cut of
                 // the brick, footprint())
-                constexpr int NB = (MODE == 2 || MODE == 4) ? 2 : 1;
-                constexpr bool CLIP = MODE >= 3;  // rows off the detector: weight 0
+                constexpr int NB = (MODE & 3) ? (MODE & 3) : 1;  // (MODE 0: unused)
+                constexpr bool CLIP = MODE >= 4;  // rows off the detector: weight 0
                 const float sh = corr ? r.shw : 0.f;
                 const float uh = fmaf(v.dz, r.kc, v.u0h);
                 const uint32_t cbase = tbase + 4u * uint32_t((r.n - tn0) * tstride - tm0);
@@ -755,7 +755,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                         // margin); the dropped ones write 0 to any tile slot
                         a = tbase + 4u * (uint32_t((r.n - tn0) * tstride) + min(uint32_t(m - tm0), trm1));
                         w = unsigned(m) < unsigned(rows) ? w : 0.f;
-                    } else if (NB == 2 && nrow == 2) {
+                    } else if (NB >= 2 && nrow == NB) {
                         a = tbase + 4u * min(uint32_t((r.n - tn0) * tstride + m - tm0),
                                              uint32_t((r.n - tn0) * tstride) + trm1);
                     }
@@ -812,12 +812,16 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             const int mode = s.walk_mode;
             if (mode == 1)
                 vphase(std::integral_constant<int, 1>{});
-            else if (mode == 3)
-                vphase(std::integral_constant<int, 3>{});
+            else if (mode == 5)
+                vphase(std::integral_constant<int, 5>{});
             else if (mode == 2)
                 vphase(std::integral_constant<int, 2>{});
-            else if (mode == 4)
-                vphase(std::integral_constant<int, 4>{});
+            else if (mode == 6)
+                vphase(std::integral_constant<int, 6>{});
+            else if (mode == 3)
+                vphase(std::integral_constant<int, 3>{});
+            else if (mode == 7)
+                vphase(std::integral_constant<int, 7>{});
             else
                 vphase(std::integral_constant<int, 0>{});
         }
