@@ -27,6 +27,7 @@
 // shared copy of the image footprint.
 #include <algorithm>
 
+#include "cvp_device.cuh"  // ColumnAnchor / anchor_at: the voxel-local float32 chi2 anchor
 #include "kernels.hpp"
 
 namespace cvpb {
@@ -51,6 +52,7 @@ constexpr int NH = BK / 32;   // voxels per lane along x3
 #define TT_MINB 4             // resident CTAs per SM (64 registers; measured faster than 3 at 80)
 #endif
 static_assert(NCOL < NT, "warps past the columns stage the tile");
+static_assert(NT - BK > NCOL, "per-layer dz threads lie past the column and footprint threads");
 constexpr int MAXN = 6;       // transaxial footprint width cached per column
 constexpr int MUS = BK + 1;
 
@@ -70,7 +72,9 @@ struct TTParams {
 struct TTSmem {
     float f1[MAXN * NCOL];    // pixel-averaged transaxial footprint per column n0 + q
     int n0[NCOL], nn[NCOL];   // first detector column, count
-    double Q0[NCOL];          // f / (b2 D0) at the base-centre depth
+    double Q0[NCOL];          // f / (b2 D0) at the base-centre depth (forward anchor)
+    int4 anchor[NCOL];        // backward: ColumnAnchor {M0, f0, dh, dl} of the column's voxels
+    float dz[BK];             // zc - s3 of the brick's voxel layers under this view
     float4 ax[NCOL];          // {dz coefficient at near depth, at far depth, h-term near, h-term far}
     float2 amp[NCOL];         // {l_phi0, 1/(u0^2 + f^2)}
     float vox[NCOL * MUS];
@@ -208,7 +212,9 @@ __device__ WideColumn wide_column(const ViewConst& vc, const Scene& sc, int i, i
 // while warps 4-7 bound the brick's detector footprint and stage the tile
 // (named barrier); each lane then carries the voxels kk = lane, lane + 32 of
 // a column through the axial walk.
-template <bool FWD>
+// AMP2: amplitude A2 (per-row elevation) rather than A1 — a template flag so
+// the unused one costs nothing in the row loop.
+template <bool FWD, bool AMP2>
 __global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TTSmem& s = *reinterpret_cast<TTSmem*>(smem_raw);
@@ -264,12 +270,23 @@ __global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
                 cnt = column_footprint(vc, sc, i, j, f1, nf, Q0, axc, amp, p.amplitude);
                 for (int q = 0; q < MAXN; ++q) s.f1[q * NCOL + c] = q < cnt ? f1[q] : 0.f;
                 s.Q0[c] = Q0;
+                // chi2 anchor of the column's first layer, split so the
+                // voxel loop runs in float32 (cvp_device.cuh column_anchor)
+                const ColumnAnchor an = column_anchor<true>(vc.pp2, sc.minz + (k0 + 0.5) * sc.a3 - vc.s3,
+                                                            Q0, sc.a3);
+                s.anchor[c] = make_int4(an.M0, __float_as_int(an.f0), __float_as_int(an.dh),
+                                        __float_as_int(an.dl));
                 s.ax[c] = axc;
                 s.amp[c] = amp;
             }
             s.n0[c] = nf;
             s.nn[c] = cnt;
         } else {
+            if (tid >= NT - BK) {
+                // per-layer dz of this view (float64 -> float32 once per layer)
+                const int kk = tid - (NT - BK);
+                s.dz[kk] = float(sc.minz + (k0 + kk + 0.5) * sc.a3 - vc.s3);
+            }
             if (tid == NCOL) {
                 // footprint rectangle of the brick (corner projections)
                 double cmin = INFINITY, cmax = -INFINITY, rmin = INFINITY, rmax = -INFINITY;
@@ -351,13 +368,27 @@ __global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
             const bool kvalid = k < k1;
             const float mu = FWD ? s.vox[c * MUS + kk] : 0.f;
             if (FWD && !__any_sync(0xffffffffu, kvalid && mu != 0.f)) continue;
-            const double dz64 = sc.minz + (k + 0.5) * sc.a3 - vc.s3;
-            const float dz = float(dz64);
-            // anchor chi2(zc) at the base-centre depth (float64), split
-            const double c0 = fma(-dz64, s.Q0[c], vc.pp2);
-            const double mr = rint(c0);
-            const int m_ref = int(mr);
-            const float u = float(c0 - mr), pm = float(vc.pp2 - mr);
+            const float dz = s.dz[kk];
+            // anchor chi2(zc) at the base-centre depth: integer row m_ref and
+            // float32 remainders u = chi2 - m_ref, pm = pp2 - m_ref
+            int m_ref;
+            float u, pm;
+            if (FWD) {
+                // float64 per voxel (the float32 split below measured 3% slower
+                // here: its extra live state spills in the forward)
+                const double c0 = fma(-(sc.minz + (k + 0.5) * sc.a3 - vc.s3), s.Q0[c], vc.pp2);
+                const double mr = rint(c0);
+                m_ref = int(mr);
+                u = float(c0 - mr);
+                pm = float(vc.pp2 - mr);
+            } else {
+                // the column's float64 split, float32 per voxel (exact to
+                // ~1e-7 px; cvp_device.cuh anchor_at): backward +6%
+                const int4 a4 = s.anchor[c];
+                const ColumnAnchor an{a4.x, __int_as_float(a4.y), __int_as_float(a4.z), __int_as_float(a4.w)};
+                float Mf_unused;
+                anchor_at(an, float(vc.pp2), float(kk), m_ref, Mf_unused, u, pm);
+            }
             const float4 axc = s.ax[c];
             float t0 = u + dz * axc.x - axc.z, t1 = u + dz * axc.x + axc.z;
             float t2 = u + dz * axc.y - axc.w, t3 = u + dz * axc.y + axc.w;
@@ -377,7 +408,7 @@ __global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
                 const float c3 = fminf(fmaxf(x, t2), t3);
                 return (c1 - t0) * (c1 - t0) * r1 + mid + (c3 - t2) * (w3 + t3 - c3) * r3;
             };
-            const float ampA1 = amp.x * sqrtf(1.f + (u - pm) * (u - pm) * b2 * b2 * amp.y);
+            const float ampA1 = AMP2 ? 0.f : amp.x * sqrtf(1.f + (u - pm) * (u - pm) * b2 * b2 * amp.y);
             float acc = 0.f;
             const bool active = kvalid && (!FWD || mu != 0.f);
             const float muq = FWD ? mu * s.qscale : 0.f;  // fixed-point scale folded into mu
@@ -392,7 +423,7 @@ __global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
                     g_prev = g;
                     if (!(f2 > 0.f)) continue;
                     float a;
-                    if (p.amplitude) {
+                    if (AMP2) {
                         const float vm = float(m - m_ref) - pm;  // (m - pp2)
                         a = amp.x * sqrtf(1.f + vm * vm * b2 * b2 * amp.y);
                     } else {
@@ -401,12 +432,16 @@ __global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
                     const float wrow = a * f2;
                     if (inside) {
                         const int off = (nfirst - tn0) * tstride + (m - tm0);
-                        for (int q = 0; q < ncache; ++q) {
-                            const float w = wrow * s.f1[q * NCOL + c];
-                            if (FWD)
-                                red_s32(itile + off + q * tstride, __float2int_rn(muq * w));
-                            else
-                                acc = fmaf(w, tile[off + q * tstride], acc);
+                        // unrolled: ncache is the column's (warp-uniform) width
+#pragma unroll
+                        for (int q = 0; q < MAXN; ++q) {
+                            if (q < ncache) {
+                                const float w = wrow * s.f1[q * NCOL + c];
+                                if (FWD)
+                                    red_s32(itile + off + q * tstride, __float2int_rn(muq * w));
+                                else
+                                    acc = fmaf(w, tile[off + q * tstride], acc);
+                            }
                         }
                     } else {
                         for (int q = 0; q < ncache; ++q) {
@@ -438,7 +473,7 @@ __global__ void __launch_bounds__(NT, TT_MINB) tt_brick_kernel(TTParams p) {
                     g_prev = g;
                     if (!(f2 > 0.f)) continue;
                     const float vm = float(m - m_ref) - pm;
-                    const float a = p.amplitude ? amp.x * sqrtf(1.f + vm * vm * b2 * b2 * amp.y) : ampA1;
+                    const float a = AMP2 ? amp.x * sqrtf(1.f + vm * vm * b2 * b2 * amp.y) : ampA1;
                     float h_prev = trap_cdf(float(wc.nlo) - 0.5f, wc.s0, wc.s1, wc.s2, wc.s3);
                     for (int nn = wc.nlo; nn <= wc.nhi; ++nn) {
                         const float hh = trap_cdf(float(nn) + 0.5f, wc.s0, wc.s1, wc.s2, wc.s3);
@@ -525,17 +560,19 @@ cudaError_t launch_tt(const TTLaunch& L, bool forward, cudaStream_t stream) {
         e = cudaMemsetAsync(L.proj_out, 0, sizeof(float) * size_t(sc.rows) * sc.cols * L.view_count,
                             stream);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(tt_brick_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        auto kern = L.amplitude ? tt_brick_kernel<true, true> : tt_brick_kernel<true, false>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         if (e != cudaSuccess) return e;
-        tt_brick_kernel<true><<<grid, NT, dyn, stream>>>(p);
+        kern<<<grid, NT, dyn, stream>>>(p);
     } else {
         if (groups > 1 && !L.accumulate) {
             e = cudaMemsetAsync(L.vol_out, 0, sizeof(float) * size_t(sc.n1) * sc.n2 * sc.n3, stream);
             if (e != cudaSuccess) return e;
         }
-        e = cudaFuncSetAttribute(tt_brick_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        auto kern = L.amplitude ? tt_brick_kernel<false, true> : tt_brick_kernel<false, false>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         if (e != cudaSuccess) return e;
-        tt_brick_kernel<false><<<grid, NT, dyn, stream>>>(p);
+        kern<<<grid, NT, dyn, stream>>>(p);
     }
     return cudaGetLastError();
 }
