@@ -380,7 +380,10 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     L.accumulate = accumulate;
     L.deterministic = exec ? exec->deterministic : 0;
     L.tile_need = ctx->cvp_tile_need;
-    L.tall_voxels = ctx->voxel_rows > 1.4 ? 1 : 0;
+    // the three-row straight-line general walk for voxels ~2 rows tall: the
+    // forward only (since the three-boundary fast walk took most such bricks,
+    // the backward is 3% faster at c2 without its register pressure)
+    L.tall_voxels = forward && ctx->voxel_rows > 1.4 ? 1 : 0;
     const void* table_before = ctx->d_cut_table.p;
     CVPB_TRY(reserve_cut_table(ctx, view_count, L.cut_table, L.cut_table_bytes));
     // reuse the resident table when it covers this launch's views with the
