@@ -212,6 +212,7 @@ struct cvpb_context {
     // 1 = shape B, 2 = shape C; chosen by timing them on the scene's first launch
     std::map<int, int> cvp_shape;
     double r_min = 0.0;       // smallest source-to-volume-box distance over the views
+    double z_far = 0.0;       // largest |z - s3| of the volume box over the views
     double voxel_rows = 0.0;  // mean voxel height in detector rows at the volume centre
     DevBuf<ViewConst> d_views;
     DevBuf<float> d_scale_cos, d_scale_exact;
@@ -375,6 +376,17 @@ int run_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts, const cvpb_exec_pol
     // c3 on a noise-like stack, tests/test_config_parity_gpu.py).
     L.exact = 1;
     L.relaxed = opts->precision == CVPB_PRECISION_RELAXED ? 1 : 0;
+    // relaxed CutCentroid takes one radius per voxel-cut where a brick's
+    // bound allows it (kernel footprint()); the variant is only launched for
+    // scenes where most bricks qualify (scene bound below; c3 does, the tall
+    // configs[3] / [4] volumes do not and keep the per-row kernel)
+    {
+        const double h = 0.5 * ctx->vol.voxel_size[2];
+        L.cut_radius_ok = L.relaxed && ctx->r_min > 0.0 &&
+                                  2.0 * (ctx->z_far + h) * h <= 5e-6 * ctx->r_min * ctx->r_min
+                              ? 1
+                              : 0;
+    }
     L.elevation_correction = opts->elevation_correction ? 1 : 0;
     L.cut_centroid = opts->r_estimate == CVPB_R_CUT_CENTROID ? 1 : 0;
     L.accumulate = accumulate;
@@ -757,6 +769,7 @@ int cvpb_set_geometry(cvpb_context* ctx, const cvpb_volume_geometry* vol,
             d2 += t * t;
         }
         ctx->r_min = v == 0 ? std::sqrt(d2) : std::min(ctx->r_min, std::sqrt(d2));
+        ctx->z_far = std::max(v == 0 ? 0.0 : ctx->z_far, std::max(std::abs(lo[2] - s[2]), std::abs(hi[2] - s[2])));
         // every voxel-base corner is a convex combination of the box's base
         // corners and depth is affine, so checking the 4 box corners decides
         // the reference's per-voxel depth test (cvp.cpp:82-84) for all voxels

@@ -454,11 +454,17 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
 // exactly -h at the interior boundaries below it, i.e. zero-share rows.
 // Rows m_first .. m_first + NB are emitted in order with
 // max(share, 0) * inv_r2 * wscale (the caller's mu * area, folded in here).
-template <int NB, class Emit>
+// CUTR (relaxed precision, CutCentroid): one radius per voxel-cut — the
+// cut's horizontal distance and the voxel's centre height — instead of one
+// per row segment; the launch allows it only where that changes 1/r^2 by
+// <= 2.5e-6 relative (cvp_kernels.cu footprint()).
+template <int NB, class Emit, bool CUTR = false>
 __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh, float pmh, float dz,
                                                float h, float sh, const bool per_row_r,
                                                float inv_r2_fixed, float wscale, Emit&& emit) {
     static_assert(NB >= 1 && NB <= 3, "one to three interior boundaries");
+    if (CUTR && per_row_r) inv_r2_fixed = fast_rcp(fmaf(dz, dz, c.rho2));
+    constexpr bool PRR = !CUTR;  // per-row radius (CutCentroid, cvp.cpp:223-229)
     constexpr float kMagic = 12582912.f;
     constexpr int kMagicBits = 0x4B400000;
     const float tr = fmaf(fabsf(dz), c.tr_b, c.tr_a);
@@ -473,7 +479,7 @@ __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh
         const float t1 = clamp_mean_local(a1, sh * fabsf(pmh - e1), h);
         // weight of a record = max(share, 0) * inv_r2 * wscale
         float2 I = make_float2(inv_r2_fixed * wscale, inv_r2_fixed * wscale);
-        if (per_row_r) {
+        if (PRR && per_row_r) {
             // midpoints of the plain row segments [p1, h] and [-h, p1] (cvp.cpp:223-229)
             const float2 Z = fma2(make_float2(p1, p1), make_float2(0.5f, 0.5f),
                                   make_float2(dz + 0.5f * h, dz - 0.5f * h));
@@ -504,7 +510,7 @@ __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh
         if constexpr (NB == 2) {
             float2 I = make_float2(inv_r2_fixed * wscale, inv_r2_fixed * wscale);
             float i2 = I.x;
-            if (per_row_r) {
+            if (PRR && per_row_r) {
                 const float2 Z = fma2(add2(make_float2(h, p1), make_float2(p1, p2)),
                                       make_float2(0.5f, 0.5f), make_float2(dz, dz));
                 const float z2 = fmaf(0.5f, p2 - h, dz);
@@ -524,7 +530,7 @@ __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh
             const float t3 = clamp_mean_local(a3, sh * fabsf(pmh - e3), h);
             const float2 S2 = make_float2(T.y - t3, t3 + h);
             float2 I = make_float2(inv_r2_fixed * wscale, inv_r2_fixed * wscale), I2 = I;
-            if (per_row_r) {
+            if (PRR && per_row_r) {
                 const float2 Z = fma2(add2(make_float2(h, p1), make_float2(p1, p2)),
                                       make_float2(0.5f, 0.5f), make_float2(dz, dz));
                 const float2 Z2 = fma2(add2(make_float2(p2, p3), make_float2(p3, -h)),

@@ -342,9 +342,11 @@ __device__ __noinline__ float offtile_walk(CutRec r, int Mi, float Mf, float uh,
     return cut_acc;
 }
 
-// CORR: elevation correction option; CCR: CutCentroid radius estimate
-// (cvp.hpp:17-22) — compile-time so the unused paths cost no registers.
-template <bool EXACT, bool FWD, bool CORR, bool CCR, int NR>
+// CORR: elevation correction option; CCR: radius estimate (cvp.hpp:17-22):
+// 0 VoxelCenter, 1 CutCentroid per row segment, 2 CutCentroid in relaxed
+// precision (per voxel-cut where the brick allows it) — compile-time so the
+// unused paths cost no registers.
+template <bool EXACT, bool FWD, bool CORR, int CCR, int NR>
 __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
     const int rows = sc.rows, cols = sc.cols;
     const size_t npx = size_t(rows) * cols;
     const float h = p.h;
-    constexpr bool corr = CORR, per_row_r = CCR;
+    constexpr bool corr = CORR, per_row_r = CCR != 0;
 
     for (int v = vg0; v < vg1; ++v) {
         const ViewConst& vc = p.views[v];
@@ -504,6 +506,15 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                             mode += 4;
                         }
                     }
+                }
+                // relaxed CutCentroid: one radius per voxel-cut where that
+                // changes no record's 1/r^2 by more than 5e-6 relative: the
+                // row-segment midpoints lie within h of the voxel centre, so
+                // |d ln(1/r^2)| <= 2 (|dz|max + h) h / dmin^2
+                if (CCR == 2 && mode != 0) {
+                    const float hh = 0.5f * float(sc.a3);
+                    const float zm = fmaxf(fabsf(zlo), fabsf(zhi)) + hh;
+                    if (2.f * zm * hh <= 5e-6f * dmin * dmin) mode |= 8;
                 }
                 s.walk_mode = mode;
             }
@@ -743,7 +754,8 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 // (fast mode: the elevation gate holds for every voxel-cut of
                 // the brick, footprint())
                 constexpr int NB = (MODE & 3) ? (MODE & 3) : 1;  // (MODE 0: unused)
-                constexpr bool CLIP = MODE >= 4;  // rows off the detector: weight 0
+                constexpr bool CLIP = (MODE & 4) != 0;  // rows off the detector: weight 0
+                constexpr bool CUTR = (MODE & 8) != 0;  // relaxed: one radius per voxel-cut
                 const float sh = corr ? r.shw : 0.f;
                 const float uh = fmaf(v.dz, r.kc, v.u0h);
                 const uint32_t cbase = tbase + 4u * uint32_t((r.n - tn0) * tstride - tm0);
@@ -766,7 +778,8 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                         v.acc = fmaf(lds_f32(a), w, v.acc);
                 };
                 const float ws = FWD ? v.muq * r.A : r.A;
-                walk_rows_fast<NB>(r, v.Mi, uh, v.pmh, v.dz, h, sh, per_row_r, v.inv_r2_fixed, ws, emit);
+                walk_rows_fast<NB, decltype(emit)&, CUTR>(r, v.Mi, uh, v.pmh, v.dz, h, sh, per_row_r,
+                                                          v.inv_r2_fixed, ws, emit);
             };
             auto cut = [&](const CutRec& r) {
                 if (tile_ok && unsigned(r.n - tn0) < unsigned(tcols)) {
@@ -810,20 +823,28 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
         };
         {
             const int mode = s.walk_mode;
-            if (mode == 1)
-                vphase(std::integral_constant<int, 1>{});
-            else if (mode == 5)
-                vphase(std::integral_constant<int, 5>{});
-            else if (mode == 2)
-                vphase(std::integral_constant<int, 2>{});
-            else if (mode == 6)
-                vphase(std::integral_constant<int, 6>{});
-            else if (mode == 3)
-                vphase(std::integral_constant<int, 3>{});
-            else if (mode == 7)
-                vphase(std::integral_constant<int, 7>{});
+            auto dispatch = [&](auto cutr_tag) {
+                constexpr int C = decltype(cutr_tag)::value;  // 0, or 8 (per-cut radius)
+                const int m = mode & 7;
+                if (m == 1)
+                    vphase(std::integral_constant<int, 1 | C>{});
+                else if (m == 5)
+                    vphase(std::integral_constant<int, 5 | C>{});
+                else if (m == 2)
+                    vphase(std::integral_constant<int, 2 | C>{});
+                else if (m == 6)
+                    vphase(std::integral_constant<int, 6 | C>{});
+                else if (m == 3)
+                    vphase(std::integral_constant<int, 3 | C>{});
+                else if (m == 7)
+                    vphase(std::integral_constant<int, 7 | C>{});
+                else
+                    vphase(std::integral_constant<int, 0>{});
+            };
+            if (CCR == 2 && (mode & 8))
+                dispatch(std::integral_constant<int, CCR == 2 ? 8 : 0>{});
             else
-                vphase(std::integral_constant<int, 0>{});
+                dispatch(std::integral_constant<int, 0>{});
         }
         // ---- flush (forward) ----------------------------------------------
         // Lanes cover a power-of-two span of tile columns (coalesced float
@@ -1087,7 +1108,7 @@ __global__ void cut_records_kernel(Scene sc, const ViewConst* views, int view, i
     *n_out = count;
 }
 
-template <bool EXACT, bool FWD, bool CORR, bool CCR, int NR>
+template <bool EXACT, bool FWD, bool CORR, int CCR, int NR>
 cudaError_t launch_variant(const CvpParams& p, dim3 grid, int dyn, cudaStream_t stream) {
     cudaError_t e = cudaFuncSetAttribute(cvp_brick_kernel<EXACT, FWD, CORR, CCR, NR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
@@ -1100,12 +1121,17 @@ cudaError_t launch_variant(const CvpParams& p, dim3 grid, int dyn, cudaStream_t 
 // correction, CutCentroid radius); other option sets walk two.
 template <bool EXACT, bool FWD>
 cudaError_t launch_opts(const CvpParams& p, dim3 grid, int dyn, bool tall, cudaStream_t stream) {
-    if (p.corr)
-        return p.per_row_r ? (tall ? launch_variant<EXACT, FWD, true, true, 3>(p, grid, dyn, stream)
-                                   : launch_variant<EXACT, FWD, true, true, 2>(p, grid, dyn, stream))
-                           : launch_variant<EXACT, FWD, true, false, 2>(p, grid, dyn, stream);
-    return p.per_row_r ? launch_variant<EXACT, FWD, false, true, 2>(p, grid, dyn, stream)
-                       : launch_variant<EXACT, FWD, false, false, 2>(p, grid, dyn, stream);
+    if (p.corr) {
+        if (p.per_row_r == 2)
+            return tall ? launch_variant<EXACT, FWD, true, 2, 3>(p, grid, dyn, stream)
+                        : launch_variant<EXACT, FWD, true, 2, 2>(p, grid, dyn, stream);
+        return p.per_row_r ? (tall ? launch_variant<EXACT, FWD, true, 1, 3>(p, grid, dyn, stream)
+                                   : launch_variant<EXACT, FWD, true, 1, 2>(p, grid, dyn, stream))
+                           : launch_variant<EXACT, FWD, true, 0, 2>(p, grid, dyn, stream);
+    }
+    if (p.per_row_r == 2) return launch_variant<EXACT, FWD, false, 2, 2>(p, grid, dyn, stream);
+    return p.per_row_r ? launch_variant<EXACT, FWD, false, 1, 2>(p, grid, dyn, stream)
+                       : launch_variant<EXACT, FWD, false, 0, 2>(p, grid, dyn, stream);
 }
 
 // The per-(view, column) cut table (BandCutter + compute_cuts + fill_cut_info,
@@ -1224,7 +1250,8 @@ cudaError_t CVP_PUB(launch_cvp)(const CvpLaunch& L, cudaStream_t stream) {
     p.views = L.views;
     p.scales = L.scales;
     p.corr = L.elevation_correction;
-    p.per_row_r = L.cut_centroid;
+    // relaxed precision + CutCentroid: the per-voxel-cut radius where allowed
+    p.per_row_r = L.cut_centroid ? (L.relaxed && L.cut_radius_ok ? 2 : 1) : 0;
     p.h = float(0.5 * sc.a3);
     p.tile_cap = tile_cap;
     // CVPB_NO_TILE=1: every record takes the global (float-atomic / direct

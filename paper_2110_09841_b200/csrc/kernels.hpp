@@ -19,6 +19,7 @@ struct CvpLaunch {
     int view_begin, view_count;
     int forward, exact, elevation_correction, cut_centroid;
     int relaxed;              // CvpPrecision::Single (same geometry, see run_cvp)
+    int cut_radius_ok = 0;    // relaxed CutCentroid: per-voxel-cut radius kernel (run_cvp)
     int accumulate, deterministic;
     int tile_need;            // largest brick footprint (floats), see launch_cvp_tile_need
     int tall_voxels;          // voxels ~2 detector rows tall: three straight-line rows
