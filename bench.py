@@ -388,6 +388,31 @@ def run_native(args):
     value = work / (ms_per_step * 1e-3)
     del b_all
 
+    # the other precision of the same P + BP (BASELINE configs[2] names exact
+    # and relaxed): device-timed like the headline, 2 warm + 3 timed steps,
+    # reported beside it (N = 1 only; the headline stays args.precision)
+    other = None
+    if world == 1 and not args.no_other_precision:
+        oprec = "relaxed" if args.precision == "exact" else "exact"
+        oopts = cb.CvpOptions(precision=cb.CvpPrecision.Double if oprec == "exact"
+                              else cb.CvpPrecision.Single)
+        oe = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        pms, bms = [], []
+        for it in range(5):
+            oe[0].record(stream)
+            scene.project_cvp(x, p, oopts, view_begin=v0, view_count=v1 - v0)
+            oe[1].record(stream)
+            scene.backproject_cvp(b, bp, oopts, view_begin=v0, view_count=v1 - v0)
+            oe[2].record(stream)
+            torch.cuda.synchronize()
+            if it >= 2:
+                pms.append(oe[0].elapsed_time(oe[1]))
+                bms.append(oe[1].elapsed_time(oe[2]))
+        opm, obm = statistics.mean(pms), statistics.mean(bms)
+        other = {"precision": oprec, "value": work / ((opm + obm) * 1e-3), "unit": UNIT,
+                 "p_gvps": work / (opm * 1e-3), "bp_gvps": work / (obm * 1e-3), "steps": 3,
+                 "how": "same P + BP, device-timed with CUDA events after 2 warm-up steps"}
+
     # ---- e2e through the reference-facing C-ABI host path ------------------
     # N = 1: cvpb_project_cvp_host + cvpb_backproject_cvp_host (project_cvp_into /
     # backproject_cvp_into with float64 host buffers). N > 1, per rank, on a
@@ -581,7 +606,8 @@ def run_native(args):
                # shape timed) in the warm-up and is reused; the stack memset is a
                # cudaMemsetAsync
                "gpu_launches": 3 * args.steps,
-               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk}
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+               "other_precision": other}
         print(json.dumps(out))
         sys.stdout.flush()
     if world > 1:
@@ -600,6 +626,7 @@ def main():
                     help="reference arm: sample views per step (P + BP each)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-other-precision", action="store_true")
     ap.add_argument("--cgls-iters", type=int, default=10,
                     help="device-resident CGLS iterations timed for cgls.ms_per_iter (0 = skip)")
     ap.add_argument("--selftest-spawn", action="store_true", help=argparse.SUPPRESS)

@@ -15,6 +15,6 @@ done
 unset CVPB_CVP_SHAPE
 if [ "${LAUNCHES:-1}" = 1 ]; then
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    --log-file gpurun_out/launches_${tag}.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline \
+    --log-file gpurun_out/launches_${tag}.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-other-precision \
     --cgls-iters 0 > gpurun_out/bench_ncu_${tag}.log 2>&1
 fi
