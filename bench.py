@@ -587,6 +587,11 @@ def run_native(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cpu = cpu_baseline_sample(args.precision, per_step=2, steps=2)
+            # the reference's other precision (report Double and
+            # Single), a smaller sample: one step of 2 views
+            oc = cpu_baseline_sample("relaxed" if args.precision == "exact" else "exact",
+                                     per_step=2, steps=1)
+            cpu["other_precision"] = {k: oc[k] for k in ("value", "p_gvps", "bp_gvps", "sample")}
         except Exception as e:  # the checker library may be absent on a fresh box
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
                    "sample": str(e)[:200]}
