@@ -297,6 +297,16 @@ def run_native(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     coll_dev = "cpu" if share else "cuda"  # device of the small timing all-reduces
 
+    def reduce_scatter(out, full):
+        # NCCL reduce-scatter; gloo (the shared-GPU code-path check) has no
+        # CUDA reduce-scatter, so it all-reduces a host copy and slices
+        if not share:
+            dist.reduce_scatter_tensor(out, full)
+            return
+        h = full.cpu()
+        dist.all_reduce(h)
+        out.copy_(h[rank * out.numel():(rank + 1) * out.numel()])
+
     c = CONFIG
     det = cb.DetectorGeometry.make(c["rows"], c["cols"], c["pw"], c["ph"])
     geom = cb.VolumeGeometry.make(c["counts"], c["voxel"])
@@ -347,7 +357,7 @@ def run_native(args):
         if peers is not None:
             peers._barrier()  # every rank's adds have landed in this rank's slab
         elif world > 1:
-            dist.reduce_scatter_tensor(slab, bp.view(-1))
+            reduce_scatter(slab, bp.view(-1))
         if ev:
             ev[3].record(stream)
 
@@ -447,7 +457,7 @@ def run_native(args):
                 N.check(L.cvpb_backproject_cvp_host_partial(
                     shard._h, C.byref(opts._c()), C.byref(ex._c()), C.c_void_p(b64n.ctypes.data),
                     C.c_void_p(bp.data_ptr()), st))
-                dist.reduce_scatter_tensor(slab, bp.view(-1))
+                reduce_scatter(slab, bp.view(-1))
                 N.check(L.cvpb_vec_to_host64(shard._h, C.c_void_p(slab.data_ptr()),
                                              C.c_void_p(o64n.ctypes.data), slab.numel(), st))
 
