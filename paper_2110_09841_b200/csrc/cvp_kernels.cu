@@ -658,6 +658,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
         }
         // ---- V-phase -----------------------------------------------------
         const float pp2f = float(vc.pp2);
+        const float pp2h = pp2f + 0.5f;
         const float qs = FWD ? s.qscale : 0.f;
         // Forward, off-tile cuts: the view's image pointer is re-read from
         // shared memory inside that rare branch so no 64-bit address stays
@@ -681,7 +682,9 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(a4.x), "=r"(a4.y), "=r"(a4.z), "=r"(a4.w)
                          : "r"(sbase + uint32_t(offsetof(Smem, anchor)) + 16u * c));
-            const ColumnAnchor an{a4.x, __int_as_float(a4.y), __int_as_float(a4.z),
+            // (+1/2 row shift of the walk folded into the anchor remainder and
+            // pp2 once per column instead of per voxel)
+            const ColumnAnchor an{a4.x, __int_as_float(a4.y) + 0.5f, __int_as_float(a4.z),
                                   __int_as_float(a4.w)};
             VoxState vs[NV];
             bool any_active = false;
@@ -697,18 +700,18 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 v.mu = FWD ? lds_f32(v.vaddr) : 0.f;
                 v.active = v.kvalid && (!FWD || v.mu != 0.f);
                 any_active |= v.active;
-                float u0, pm;
                 float Mf;  // == float(v.Mi) exactly: not kept (one register per voxel)
-                anchor_at(an, pp2f, float(kk), v.Mi, Mf, u0, pm);
-                v.u0h = u0 + 0.5f;
-                v.pmh = pm + 0.5f;
+                anchor_at(an, pp2h, float(kk), v.Mi, Mf, v.u0h, v.pmh);
                 v.muq = v.mu * qs;  // forward: fixed-point scale folded into mu
                 v.inv_r2_fixed = per_row_r ? -1.f
                                            : fast_rcp(lds_f32(sbase + uint32_t(offsetof(Smem, rho2c)) + 4u * c) +
                                                       v.dz * v.dz);
                 v.acc = 0.f;
             }
-            if (FWD && !__any_sync(0xffffffffu, any_active)) continue;
+            // (one voxel group per column: the column's nonzero flag, which
+            // zeroed its cut count in the G-phase, already guarantees an
+            // active voxel)
+            if (FWD && NG > 1 && !__any_sync(0xffffffffu, any_active)) continue;
             // One voxel-cut. TILE: the cut's column lies in the detector tile.
             // Every row with a nonzero share then lies inside the tile (the
             // footprint is conservative by >= 1 row, brick_footprint); rows
