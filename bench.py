@@ -346,16 +346,13 @@ def run_native(args):
         if ev:
             ev[1].record(stream)
         if peers is not None:
-            peers.own.zero_()
-            peers._barrier()  # every slab zeroed before anyone adds
-            scene.backproject_cvp_scatter(b, peers.ptrs, peers.bounds, opts, view_begin=v0,
-                                          view_count=v1 - v0)
+            peers.scatter(b, opts, v0, v1 - v0)  # (barrier: receive regions free)
         else:
             scene.backproject_cvp(b, bp, opts, view_begin=v0, view_count=v1 - v0)
         if ev:
             ev[2].record(stream)
         if peers is not None:
-            peers._barrier()  # every rank's adds have landed in this rank's slab
+            peers.finish()  # barrier: every rank's stores landed; own slab = ordered sum
         elif world > 1:
             reduce_scatter(slab, bp.view(-1))
         if ev:
@@ -614,7 +611,7 @@ def run_native(args):
                "data": "synthetic",
                "config": config_dict(args, world),
                "p_ms": pm, "bp_ms": bm, "cgls": cgls, "reduce_scatter_ms": rm if world > 1 else 0.0,
-               "exchange": ("none" if world == 1 else "fused backprojection + reduce-scatter (CUDA IPC slabs, NVLink atomics)" if peers is not None else "NCCL reduce_scatter_tensor"),
+               "exchange": ("none" if world == 1 else "fused backprojection + reduce-scatter (stores into CUDA IPC receive regions over NVLink, ordered local sums)" if peers is not None else "NCCL reduce_scatter_tensor"),
                "p_gvps": work / world / (pm * 1e-3), "bp_gvps": work / world / (bm * 1e-3),
                # per step: cvp_brick_kernel<FWD> + apply_scale_kernel, cvp_brick_kernel<BWD>
                # (profiles/launches_r0*.csv); the cut table was built (and the brick

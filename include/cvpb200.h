@@ -171,20 +171,29 @@ int cvpb_backproject_cvp(cvpb_context* ctx, const cvpb_cvp_options* opts,
                          int view_begin, int view_count, int accumulate, void* stream);
 
 /* Backprojection fused with the reduce-scatter of a view-sharded job (SURVEY
- * §8e): each brick's accumulated voxels are added with float atomics straight
- * into the buffer that owns their z-plane — typically another GPU's memory,
- * reached over NVLink peer access — as soon as the brick has walked its
- * views, so the exchange overlaps the bricks still computing and no partial
- * volume is materialized. Planes [plane_begin[t], plane_begin[t+1]) go to
- * slab[t] (its element 0 is the first voxel of plane plane_begin[t]);
- * plane_begin[0] = 0, plane_begin[n] = N3. The caller zeroes the slabs (or
- * holds sums to add to) and orders them against this stream. The atomic
- * order varies run to run: ExecPolicy::deterministic is refused. */
+ * §8e): each brick's voxels go straight into the buffer that owns their
+ * z-plane — typically another GPU's memory, reached over NVLink peer access —
+ * as soon as the brick has walked its views, so the exchange overlaps the
+ * bricks still computing and no partial volume is materialized. Planes
+ * [plane_begin[t], plane_begin[t+1]) go to slab[t] (its element 0 is the
+ * first voxel of plane plane_begin[t]); plane_begin[0] = 0, plane_begin[n] =
+ * N3. The caller orders the slabs against this stream.
+ *   store = 1: the launch's result OVERWRITES the regions (plain stores; a
+ *     rank writes its own receive region of each owner, and the owner sums
+ *     its regions in a fixed order with cvpb_sum_slabs: deterministic);
+ *   store = 0: the result is ADDED with float atomics into regions the
+ *     caller zeroed (atomic order varies: ExecPolicy::deterministic refused). */
 typedef struct cvpb_slab_targets {
     int n; /* 1..16 */
     int plane_begin[17];
     float* slab[16];
+    int store;
 } cvpb_slab_targets;
+/* out[i] = sum over h = 0..n-1, in that order, of src[h][i] (float64
+ * accumulation), into out32 (float32) or out64 (float64) — the owner's half
+ * of the reduce-scatter above. n <= 16. Asynchronous on `stream`. */
+int cvpb_sum_slabs(cvpb_context* ctx, const float* const* src, int n, size_t count, float* out32,
+                   double* out64, void* stream);
 int cvpb_backproject_cvp_scatter(cvpb_context* ctx, const cvpb_cvp_options* opts,
                                  const cvpb_exec_policy* exec, const float* d_proj, int view_begin,
                                  int view_count, const cvpb_slab_targets* targets, void* stream);

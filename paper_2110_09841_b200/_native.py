@@ -39,7 +39,8 @@ class cvpb_exec_policy(C.Structure):
 
 
 class cvpb_slab_targets(C.Structure):
-    _fields_ = [("n", C.c_int), ("plane_begin", C.c_int * 17), ("slab", C.c_void_p * 16)]
+    _fields_ = [("n", C.c_int), ("plane_begin", C.c_int * 17), ("slab", C.c_void_p * 16),
+                ("store", C.c_int)]
 
 
 class cvpb_pixel_roi(C.Structure):
@@ -84,6 +85,7 @@ SIGNATURES = {
     "cvpb_backproject_cvp_host": (C.c_int, [_vp, _P(cvpb_cvp_options), _P(cvpb_exec_policy), _vp,
                                             _vp, _vp]),
     "cvpb_sync": (C.c_int, [_vp, _vp]),
+    "cvpb_sum_slabs": (C.c_int, [_vp, _P(C.c_void_p), C.c_int, C.c_size_t, _vp, _vp, _vp]),
     "cvpb_ipc_alloc": (C.c_int, [_vp, C.c_size_t, _P(C.c_void_p), _vp]),
     "cvpb_ipc_open": (C.c_int, [_vp, _vp, _P(C.c_void_p)]),
     "cvpb_ipc_close": (C.c_int, [_vp, _vp]),

@@ -1070,10 +1070,10 @@ int cvpb_backproject_cvp_scatter(cvpb_context* ctx, const cvpb_cvp_options* opts
                                  int view_count, const cvpb_slab_targets* targets, void* stream) {
     CVPB_TRY(check_ctx(ctx));
     if (!targets) return fail(CVPB_INVALID_ARGUMENT, "null slab targets");
-    if (exec && exec->deterministic)
+    if (exec && exec->deterministic && !targets->store)
         return fail(CVPB_INVALID_ARGUMENT,
-                    "the fused reduce-scatter adds with atomics: not bit-reproducible "
-                    "(use cvpb_backproject_cvp + a fixed-order reduction for ExecPolicy::deterministic)");
+                    "atomic slab targets are not bit-reproducible "
+                    "(store = 1 + cvpb_sum_slabs for ExecPolicy::deterministic)");
     const int n = targets->n;
     if (n < 1 || n > cvpb::kMaxSlabTargets)
         return fail(CVPB_INVALID_ARGUMENT, "slab targets: 1 to 16 slabs");
@@ -1092,9 +1092,35 @@ int cvpb_backproject_cvp_scatter(cvpb_context* ctx, const cvpb_cvp_options* opts
             return fail(CVPB_INVALID_ARGUMENT, "null slab target");
         tg.slab[t] = targets->slab[t];
     }
+    tg.store = targets->store ? 1 : 0;
     if (!d_proj && view_count > 0) return fail(CVPB_INVALID_ARGUMENT, "null projection buffer");
-    return run_cvp(ctx, opts, exec, false, nullptr, nullptr, d_proj, nullptr, view_begin, view_count, 1,
-                   static_cast<cudaStream_t>(stream), nullptr, nullptr, &tg);
+    if (view_count == 0 && tg.store) {
+        // nothing to backproject: store mode still overwrites with zeros
+        for (int t = 0; t < n; ++t) {
+            const size_t cnt = size_t(tg.plane_begin[t + 1] - tg.plane_begin[t]) * ctx->sc.n1 * ctx->sc.n2;
+            if (cnt) CVPB_CUDA(cudaMemsetAsync(tg.slab[t], 0, sizeof(float) * cnt, static_cast<cudaStream_t>(stream)));
+        }
+        return CVPB_OK;
+    }
+    return run_cvp(ctx, opts, exec, false, nullptr, nullptr, d_proj, nullptr, view_begin, view_count,
+                   tg.store ? 0 : 1, static_cast<cudaStream_t>(stream), nullptr, nullptr, &tg);
+}
+
+int cvpb_sum_slabs(cvpb_context* ctx, const float* const* src, int n, size_t count, float* out32,
+                   double* out64, void* stream) {
+    CVPB_TRY(check_ctx(ctx, false));
+    if (n < 1 || n > cvpb::kMaxMembers) return fail(CVPB_INVALID_ARGUMENT, "1 to 16 slabs");
+    if (!src || (!out32 && !out64) || (out32 && out64))
+        return fail(CVPB_INVALID_ARGUMENT, "sum_slabs: sources and exactly one output");
+    cvpb::SlabSources ss{};
+    for (int h = 0; h < n; ++h) {
+        if (!src[h] && count) return fail(CVPB_INVALID_ARGUMENT, "null slab source");
+        ss.p[h] = src[h];
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (out32) CVPB_CUDA(cvpb::launch_reduce_slab(ss, n, count, out32, st));
+    else CVPB_CUDA(cvpb::launch_reduce_slab64(ss, n, count, out64, st));
+    return CVPB_OK;
 }
 
 int cvpb_project_cvp_host(cvpb_context* ctx, const cvpb_cvp_options* opts,

@@ -36,13 +36,15 @@ struct Scene {
 
 // Backprojection fused with a reduce-scatter (cvpb_backproject_cvp_scatter):
 // planes [plane_begin[t], plane_begin[t + 1]) of the volume go to slab[t]
-// (element 0 = first voxel of plane plane_begin[t]), added with atomics —
-// slab[t] may live in another GPU's memory (peer access).
+// (element 0 = first voxel of plane plane_begin[t]) — stored (store = 1:
+// each rank writes its own receive region, the owner sums them) or added with
+// atomics; slab[t] may live in another GPU's memory (peer access).
 constexpr int kMaxSlabTargets = 16;
 struct SlabTargets {
     int n = 0;
     int plane_begin[kMaxSlabTargets + 1] = {};
     float* slab[kMaxSlabTargets] = {};
+    int store = 0;  // 1: plain stores (the launch's result overwrites the regions)
 };
 
 // Error flags raised by kernels (checked by the host after the launch).

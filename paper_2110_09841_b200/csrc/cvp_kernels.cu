@@ -910,10 +910,16 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 if (p.tg.n > 0) {
                     // fused reduce-scatter: straight into the slab that owns
                     // plane kq (another GPU's memory over NVLink), while the
-                    // other bricks are still computing
+                    // other bricks are still computing; plain stores when this
+                    // launch owns the region alone (one view group: each voxel
+                    // is written by exactly one brick)
                     int t = 0;
                     while (t + 1 < p.tg.n && kq >= p.tg.plane_begin[t + 1]) ++t;
-                    atomicAdd(p.tg.slab[t] + (off - size_t(p.tg.plane_begin[t]) * plane), val);
+                    float* dst = p.tg.slab[t] + (off - size_t(p.tg.plane_begin[t]) * plane);
+                    if (p.tg.store && !p.atomic_out)
+                        *dst = p.accumulate ? *dst + val : val;
+                    else
+                        atomicAdd(dst, val);
                     continue;
                 }
                 float* dst = p.vol_out + off;
@@ -1336,6 +1342,17 @@ cudaError_t CVP_PUB(launch_cvp)(const CvpLaunch& L, cudaStream_t stream) {
         if (!L.forward && groups > 1 && !p.accumulate && L.targets.n == 0) {
             e = cudaMemsetAsync(L.vol_out, 0, sizeof(float) * nvox, stream);
             if (e != cudaSuccess) return e;
+        }
+        if (!L.forward && groups > 1 && !p.accumulate && L.targets.n > 0 && L.targets.store) {
+            // several view groups add with atomics: the overwrite semantics
+            // of store mode start from zeroed regions (peer memory included)
+            for (int t = 0; t < L.targets.n; ++t) {
+                const size_t cnt = size_t(L.targets.plane_begin[t + 1] - L.targets.plane_begin[t]) *
+                                   size_t(sc.n1) * sc.n2;
+                if (cnt == 0) continue;
+                e = cudaMemsetAsync(L.targets.slab[t], 0, sizeof(float) * cnt, stream);
+                if (e != cudaSuccess) return e;
+            }
         }
         dim3 grid(nbricks, groups);
         // (float64 world quantities in both precisions: EXACT geometry always)

@@ -12,12 +12,13 @@
 //   forward   slab upload (H2D, float64 -> float32)  | barrier |
 //             all-gather of the other slabs (peer copies over NVLink), then
 //             the member's views -> its part of the host stack
-//   backward  fused (CVP, default): slabs zeroed | barrier | every member's
-//             bricks add their voxels straight into the owning member's slab
-//             over peer memory (cvpb_backproject_cvp_scatter: the
-//             reduce-scatter overlaps the bricks still computing, no partial
-//             volume exists) | barrier | slab -> float64 -> host;
-//             two-pass (deterministic, TT / Siddon, no peer atomics): the
+//   backward  fused (CVP, default): | barrier | every member's bricks store
+//             their voxels straight into the owning member's receive region
+//             for that source over peer memory (cvpb_backproject_cvp_scatter,
+//             store mode: the exchange overlaps the bricks still computing)
+//             | barrier | each owner sums its regions in member order
+//             (cvpb_sum_slabs, float64) -> its slab of the host volume;
+//             two-pass (TT / Siddon, no peer access): the
 //             member's part of the stack -> a full partial volume | barrier |
 //             launch_reduce_slab64 reads the member's slab out of every
 //             member's partial over peer memory, sums the members in a fixed
@@ -153,6 +154,7 @@ struct cvpb_group {
         Buf<double> stage;      // float64 staging of host transfers
         Buf<double> partials;   // dot partials
         Buf<float> gather;      // reduce-scatter without peer access: the slabs of every member
+        Buf<float> recv;        // fused backward: one slab-sized region per member (its voxels)
         Buf<int> flag;
     };
     std::vector<Member> m;
@@ -286,43 +288,57 @@ int reduce_slab(cvpb_group* g, int i, float* out32, double* out64) {
     return CVPB_OK;
 }
 
-// Backward with the reduce-scatter fused in: every member's bricks add their
-// voxels straight into the member slab that owns their planes (`slab32` of
-// each member, float32, peer memory; cvpb_backproject_cvp_scatter). CVP only,
-// not in deterministic mode (atomic order), and only with peer atomics
-// between every pair of members; CVPB_GROUP_FUSED=0 forces the two-pass path
-// (full partial volumes + fixed-order peer-load reduction).
+// Backward with the reduce-scatter fused in (CVP): every member's bricks
+// store their voxels straight into the owning member's receive buffer — one
+// slab-sized region per source member, peer memory over NVLink
+// (cvpb_backproject_cvp_scatter, store mode) — and each owner then sums its
+// regions locally in member order (cvpb_sum_slabs). Plain stores, no
+// atomics (a member's launch writes each of its voxels once), and the sum
+// order is fixed, so the result is bit-reproducible and deterministic mode is
+// served too. Needs peer access between every pair of members;
+// CVPB_GROUP_FUSED=0 forces the two-pass path (full partial volumes +
+// fixed-order peer-load reduction).
 bool fused_backward(const cvpb_group* g, const Op& op) {
-    if (op.kind != 0 || op.exec.deterministic || !g->direct_peer || !g->peer_atomics) return false;
+    if (op.kind != 0 || !g->direct_peer || !g->peer_atomics) return false;
     const char* e = std::getenv("CVPB_GROUP_FUSED");
     return !(e && e[0] == '0');
 }
 
-// slab_of(h) = member h's float32 slab buffer. Zero own slab, meet, scatter
-// this member's views into every slab, meet again: on return (stream order)
-// the member's slab holds the sum over all members.
-template <class SlabOf>
-int scatter_backward(cvpb_group* g, int i, Barrier& bar, const Op& op, const float* proj, SlabOf&& slab_of) {
+// Scatter this member's views into every owner's receive region for this
+// member, meet, then sum the own receive buffer into out32 / out64 (the
+// member's slab). Stream-ordered: on return the sum is enqueued on mb.st.
+int scatter_backward(cvpb_group* g, int i, Barrier& bar, const Op& op, const float* proj, float* out32,
+                     double* out64) {
     auto& mb = g->m[i];
     const int n = int(g->m.size());
-    if (mb.ns) G_CUDA(cudaMemsetAsync(slab_of(i), 0, sizeof(float) * mb.ns, mb.st));
+    G_CUDA(mb.recv.reserve(std::max<size_t>(mb.ns * n, 1)));
+    // the receive buffers are free (their previous sums are enqueued before)
     G_CUDA(cudaEventRecord(mb.ev_ready, mb.st));
-    G_SYNC(bar);  // every member's zeroing is recorded
+    G_SYNC(bar);
     for (int h = 0; h < n; ++h) G_CUDA(cudaStreamWaitEvent(mb.st, g->m[h].ev_ready, 0));
-    if (mb.nv) {
-        cvpb_slab_targets tg{};
-        tg.n = n;
-        const size_t plane = size_t(g->vol.counts[0]) * g->vol.counts[1];
-        for (int h = 0; h < n; ++h) {
-            tg.plane_begin[h] = int(g->m[h].s0 / plane);
-            tg.slab[h] = slab_of(h);
-        }
-        tg.plane_begin[n] = g->vol.counts[2];
-        G_TRY(cvpb_backproject_cvp_scatter(mb.ctx, &op.cvp, &op.exec, proj, mb.v0, mb.nv, &tg, mb.st));
+    cvpb_slab_targets tg{};
+    tg.n = n;
+    tg.store = 1;
+    const size_t plane = size_t(g->vol.counts[0]) * g->vol.counts[1];
+    for (int h = 0; h < n; ++h) {
+        tg.plane_begin[h] = int(g->m[h].s0 / plane);
+        tg.slab[h] = g->m[h].recv.p + size_t(i) * g->m[h].ns;  // owner h's region for source i
     }
+    tg.plane_begin[n] = g->vol.counts[2];
+    if (mb.nv)
+        G_TRY(cvpb_backproject_cvp_scatter(mb.ctx, &op.cvp, &op.exec, proj, mb.v0, mb.nv, &tg, mb.st));
+    else
+        for (int h = 0; h < n; ++h)  // no views: this source contributes zeros
+            if (g->m[h].ns)
+                G_CUDA(cudaMemsetAsync(tg.slab[h], 0, sizeof(float) * g->m[h].ns, mb.st));
     G_CUDA(cudaEventRecord(mb.ev_done, mb.st));
     G_SYNC(bar);  // every member's scatter is recorded
     for (int h = 0; h < n; ++h) G_CUDA(cudaStreamWaitEvent(mb.st, g->m[h].ev_done, 0));
+    if (mb.ns) {
+        std::vector<const float*> src(n);
+        for (int h = 0; h < n; ++h) src[h] = mb.recv.p + size_t(h) * mb.ns;
+        G_TRY(cvpb_sum_slabs(mb.ctx, src.data(), n, mb.ns, out32, out64, mb.st));
+    }
     return CVPB_OK;
 }
 
@@ -407,11 +423,14 @@ int backward_host(cvpb_group* g, const Op& op, const double* proj, double* volum
         G_TRY(run_members(g, [&](int i, Barrier& bar) -> int {
             auto& mb = g->m[i];
             G_TRY(ensure_buffers(g, i, 0));
-            G_CUDA(mb.ss.reserve(mb.ns));
             const auto t0 = std::chrono::steady_clock::now();
             G_TRY(upload(mb, proj + g->npx * size_t(mb.v0), mb.proj.p, g->npx * size_t(mb.nv)));
-            G_TRY(scatter_backward(g, i, bar, op, mb.proj.p, [&](int h) { return g->m[h].ss.p; }));
-            G_TRY(download(mb, mb.ss.p, volume + mb.s0, mb.ns));
+            // the member's slab summed in float64 straight into the staging
+            // buffer of the host download
+            G_TRY(scatter_backward(g, i, bar, op, mb.proj.p, nullptr, mb.stage.p));
+            if (mb.ns)
+                G_CUDA(cudaMemcpyAsync(volume + mb.s0, mb.stage.p, sizeof(double) * mb.ns,
+                                       cudaMemcpyDeviceToHost, mb.st));
             G_CUDA(cudaStreamSynchronize(mb.st));
             secs[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             return CVPB_OK;
@@ -457,7 +476,7 @@ int cgls_host(cvpb_group* g, const Op& op, const double* b, double* x, int itera
             return CVPB_OK;
         };
         auto adjoint_into_s = [&]() -> int {  // s slab = (A^T r) slab
-            if (fused) return scatter_backward(g, i, bar, op, r, [&](int h) { return g->m[h].ss.p; });
+            if (fused) return scatter_backward(g, i, bar, op, r, mb.ss.p, nullptr);
             G_TRY(op_backward(op, mb, g->nvox, r, mb.part.p));
             G_CUDA(cudaEventRecord(mb.ev_ready, mb.st));
             G_SYNC(bar);
@@ -536,7 +555,7 @@ int cgls_host(cvpb_group* g, const Op& op, const double* b, double* x, int itera
 void release_member(cvpb_group::Member& mb) {
     cudaSetDevice(mb.device);
     if (mb.st) cudaStreamSynchronize(mb.st);
-    for (auto* b : {&mb.vol, &mb.part, &mb.proj, &mb.q, &mb.sx, &mb.ss, &mb.gather}) b->release();
+    for (auto* b : {&mb.vol, &mb.part, &mb.proj, &mb.q, &mb.sx, &mb.ss, &mb.gather, &mb.recv}) b->release();
     mb.stage.release();
     mb.partials.release();
     mb.flag.release();

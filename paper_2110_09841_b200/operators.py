@@ -211,12 +211,14 @@ class DeviceScene:
         return out
 
     def backproject_cvp_scatter(self, proj, slabs, plane_begin, opts: CvpOptions = None,
-                                exec: ExecPolicy = None, view_begin=0, view_count=None, stream=None):
+                                exec: ExecPolicy = None, view_begin=0, view_count=None, stream=None,
+                                store=False):
         """Backprojection fused with a reduce-scatter: planes
         [plane_begin[t], plane_begin[t+1]) are added (float atomics) into
         slabs[t] — a float32 CUDA tensor or a raw device address, on this or
         another GPU with peer access — as each brick finishes
-        (cvpb_backproject_cvp_scatter)."""
+        (cvpb_backproject_cvp_scatter). store=True overwrites the regions
+        instead (plain stores; sum several ranks' regions with sum_slabs)."""
         opts = opts or CvpOptions()
         exec = exec or ExecPolicy()
         vb, vc = self._range(view_begin, view_count)
@@ -226,6 +228,7 @@ class DeviceScene:
         plane = self.vol_geom.counts[0] * self.vol_geom.counts[1]
         tg = N.cvpb_slab_targets()
         tg.n = n
+        tg.store = 1 if store else 0
         for t in range(n + 1):
             tg.plane_begin[t] = int(plane_begin[t])
         for t, sl in enumerate(slabs):
@@ -238,6 +241,24 @@ class DeviceScene:
                                                      self._stk(proj, vc), vb, vc, C.byref(tg),
                                                      _stream(stream)))
         return slabs
+
+    def sum_slabs(self, sources, count, out, stream=None):
+        """out[:count] = sum of the sources (device addresses or float32 CUDA
+        tensors) in order, float64 accumulation (cvpb_sum_slabs); out float32
+        or float64 CUDA tensor."""
+        import torch
+        n = len(sources)
+        arr = (C.c_void_p * max(n, 1))()
+        for h, src in enumerate(sources):
+            arr[h] = src if isinstance(src, int) else _ptr(src, count, at_least=True).value
+        if not out.is_cuda or not out.is_contiguous() or out.numel() < count:
+            raise InvalidArgument("sum_slabs: out must be a contiguous CUDA tensor of at least count elements")
+        o32 = C.c_void_p(out.data_ptr()) if out.dtype == torch.float32 else None
+        o64 = C.c_void_p(out.data_ptr()) if out.dtype == torch.float64 else None
+        if o32 is None and o64 is None:
+            raise InvalidArgument("sum_slabs: out must be float32 or float64")
+        N.check(N.lib().cvpb_sum_slabs(self._h, arr, n, int(count), o32, o64, _stream(stream)))
+        return out
 
     def project_cvp_host(self, vol64: np.ndarray, out64: np.ndarray = None,
                          opts: CvpOptions = None, exec: ExecPolicy = None, view_seconds=None):

@@ -13,15 +13,17 @@ Views are sharded contiguously across ranks:
   all-gathers p before each forward projection and all-reduces the float64
   dot-product scalars (solver.cpp:55-106 recurrence).
 
-For CVP the backprojection and its reduce-scatter are one kernel
-(:class:`PeerSlabs`): every rank's z-slab buffer is mapped into every other
-rank's process with CUDA IPC, and each rank's bricks add their voxels
-straight into the owning rank's slab over NVLink as they finish
-(cvpb_backproject_cvp_scatter) — no partial volume, no NCCL reduce-scatter;
-two 1-element NCCL all-reduces order the ranks' streams (slabs zeroed before
-anyone adds, all adds done before anyone reads). NCCL's reduce_scatter_tensor
-remains the path for TT / Siddon, deterministic mode, and volumes whose plane
-count the world size does not divide (``CVPB_FUSED_RS=0`` forces it).
+For CVP the backprojection and its reduce-scatter are one kernel plus a
+local sum (:class:`PeerSlabs`): every rank's receive buffer is mapped into
+every other rank's process with CUDA IPC, each rank's bricks store their
+voxels straight into the owning rank's region for that source over NVLink as
+they finish (cvpb_backproject_cvp_scatter, store mode), and each owner sums
+its regions in rank order (cvpb_sum_slabs) — no partial volume crosses the
+network after the kernel, no NCCL reduce-scatter; two 1-element NCCL
+all-reduces order the ranks' streams (regions free before anyone stores, all
+stores landed before anyone sums). NCCL's reduce_scatter_tensor remains the
+path for TT / Siddon and volumes whose plane count the world size does not
+divide (``CVPB_FUSED_RS=0`` forces it).
 
 The per-rank compute is injected (``forward_local`` / ``adjoint_local`` and a
 ``vec`` object), so the same orchestration runs over libcvpb200 on GPUs and
@@ -148,13 +150,17 @@ class _CudaBuffer:
 
 
 class PeerSlabs:
-    """The z-slabs of all ranks, each mapped into every rank's process (CUDA
-    IPC), for the fused backprojection + reduce-scatter of CVP.
+    """The receive buffers of all ranks, each mapped into every rank's process
+    (CUDA IPC), for the fused backprojection + reduce-scatter of CVP.
 
     Rank r owns planes [r * N3 / world, (r + 1) * N3 / world) (N3 divisible by
     the world size, so the slabs are the same contiguous element ranges the
-    NCCL path uses). :meth:`backproject` returns this rank's slab summed over
-    all ranks' views."""
+    NCCL path uses) and a receive buffer of world slab-sized regions, one per
+    source rank. :meth:`backproject` stores this rank's voxels of every slab
+    straight into the owners' regions for this rank (plain stores over NVLink,
+    as each brick finishes; cvpb_backproject_cvp_scatter in store mode), then
+    sums its own regions in rank order (cvpb_sum_slabs): the own slab summed
+    over all ranks' views, bit-reproducible."""
 
     def __init__(self, scene, group=None):
         import ctypes as C
@@ -175,7 +181,8 @@ class PeerSlabs:
         # not leave the others waiting in a collective): on any failure every
         # rank releases what it mapped and raises, and callers fall back to
         # the NCCL reduce-scatter
-        ok = L.cvpb_ipc_alloc(scene._h, self.elems * 4, C.byref(own), C.cast(handle, C.c_void_p)) == 0
+        ok = L.cvpb_ipc_alloc(scene._h, self.elems * 4 * self.world, C.byref(own),
+                              C.cast(handle, C.c_void_p)) == 0
         self._own_ptr = own.value if ok else None
         self._opened = []
         msgs = [None] * self.world
@@ -183,11 +190,11 @@ class PeerSlabs:
             dist.all_gather_object(msgs, (ok, bytes(handle)), group=group)
         else:
             msgs = [(ok, bytes(handle))]
-        self.ptrs = []
+        recv = []
         if all(m[0] for m in msgs):
             for r in range(self.world):
                 if r == self.rank:
-                    self.ptrs.append(self._own_ptr)
+                    recv.append(self._own_ptr)
                     continue
                 hb = (C.c_char * 64).from_buffer_copy(msgs[r][1])
                 p = C.c_void_p()
@@ -195,7 +202,7 @@ class PeerSlabs:
                     ok = False
                     break
                 self._opened.append(p.value)
-                self.ptrs.append(p.value)
+                recv.append(p.value)
         else:
             ok = False
         flags = [None] * self.world
@@ -207,8 +214,10 @@ class PeerSlabs:
             self.own = None
             self._release()
             raise RuntimeError("CUDA IPC slab mapping failed on at least one rank")
-        self.own = torch.as_tensor(_CudaBuffer(self._own_ptr, self.elems),
-                                   device=torch.device("cuda", scene.device))
+        # owner r's region for this rank (source) and this rank's own regions
+        self.ptrs = [recv[r] + self.rank * self.elems * 4 for r in range(self.world)]
+        self.sources = [self._own_ptr + h * self.elems * 4 for h in range(self.world)]
+        self.own = torch.zeros(self.elems, dtype=torch.float32, device=torch.device("cuda", scene.device))
         # device-side barrier: a 1-element NCCL all-reduce completes on every
         # rank's stream only after all ranks' earlier stream work (gloo, in
         # tests: synchronize + host barrier)
@@ -224,17 +233,26 @@ class PeerSlabs:
             torch.cuda.synchronize(self.own.device)
             dist.barrier(group=self.group)
 
-    def backproject(self, b_local, opts, view_begin, view_count, stream=None):
-        """This rank's views backprojected into every rank's slab; returns the
-        own slab (flat float32) once every rank's adds have landed."""
-        self.own.zero_()
-        self._barrier()  # every slab is zeroed before anyone adds
-        if view_count > 0:
-            self.scene.backproject_cvp_scatter(b_local, self.ptrs, self.bounds, opts,
-                                               view_begin=view_begin, view_count=view_count,
-                                               stream=stream)
-        self._barrier()  # every rank's adds are complete
+    def scatter(self, b_local, opts, view_begin, view_count, stream=None):
+        """This rank's views into every owner's receive region for this rank
+        (after a barrier: the regions' previous contents have been summed)."""
+        self._barrier()
+        self.scene.backproject_cvp_scatter(b_local, self.ptrs, self.bounds, opts,
+                                           view_begin=view_begin, view_count=view_count,
+                                           stream=stream, store=True)
+
+    def finish(self, stream=None):
+        """Barrier (every rank's stores have landed), then the own slab = the
+        own regions summed in rank order."""
+        self._barrier()
+        self.scene.sum_slabs(self.sources, self.elems, self.own, stream=stream)
         return self.own
+
+    def backproject(self, b_local, opts, view_begin, view_count, stream=None):
+        """This rank's views backprojected and reduce-scattered; returns the
+        own slab (flat float32)."""
+        self.scatter(b_local, opts, view_begin, view_count, stream)
+        return self.finish(stream)
 
     def _release(self):
         from . import _native as N
@@ -336,12 +354,13 @@ def distributed_cgls(op: DistributedOperator, b_local: torch.Tensor, iterations:
 
 def fused_reduce_scatter_ok(scene, projector: str = "cvp", exec=None, group=None) -> bool:
     """Whether the CVP backprojection can run fused with the reduce-scatter
-    (PeerSlabs): CVP, not deterministic, several ranks, N3 divisible by the
-    world size, not disabled by CVPB_FUSED_RS=0."""
+    (PeerSlabs): CVP, several ranks, N3 divisible by the world size, not
+    disabled by CVPB_FUSED_RS=0 (store mode + fixed-order sums: deterministic
+    too)."""
     import os
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    return (projector == "cvp" and world > 1 and not (exec is not None and exec.deterministic)
-            and scene.vol_geom.counts[2] % world == 0 and os.environ.get("CVPB_FUSED_RS", "1") != "0")
+    return (projector == "cvp" and world > 1 and scene.vol_geom.counts[2] % world == 0
+            and os.environ.get("CVPB_FUSED_RS", "1") != "0")
 
 
 def scene_operator(scene, opts=None, projector: str = "cvp", k_per_edge: int = 1,

@@ -11,11 +11,12 @@ Bars:
   as the single-context path -> equal to the one-context host path within
   float32 atomic reassociation (1e-6), and to the reference Double within the
   north-star bar (rel-L2 1e-5, max 1e-4);
-* backward: fused (default for CVP): every member's bricks add into the
-  owning member's slab with float atomics over peer memory; two-pass
-  (deterministic / CVPB_GROUP_FUSED=0): partials summed in a fixed member
-  order in float64 -> both within float32 reassociation of the one-context
-  result, and within the bar of the reference;
+* backward: fused (default for CVP): every member's bricks store into the
+  owning member's receive region for that source over peer memory and the
+  owner sums its regions in member order; two-pass (CVPB_GROUP_FUSED=0):
+  partials summed in a fixed member order in float64 -> both within float32
+  reassociation of the one-context result, and within the bar of the
+  reference, and both bit-reproducible;
 * CGLS: the residual history of the group equals the single-device
   device-resident CGLS (rtol 1e-5) and the reference's cgls (rtol 1e-5).
 """
@@ -208,6 +209,21 @@ def test_backproject_scatter_matches_the_device_backprojection():
         sc.backproject_cvp_scatter(proj, slabs, [0, 5, 4, 21, n3])
     with pytest.raises(InvalidArgument):
         sc.backproject_cvp_scatter(proj, slabs, bounds, exec=cb.ExecPolicy(deterministic=True))
+    # store mode overwrites whatever the regions held (plain stores), also in
+    # deterministic mode, and two sources' regions sum in order (sum_slabs)
+    for s_ in slabs:
+        s_.fill_(123.0)
+    sc.backproject_cvp_scatter(proj, slabs, bounds, store=True, exec=cb.ExecPolicy(deterministic=True))
+    torch.cuda.synchronize()
+    assert rel_l2(torch.cat(slabs, 0).double().cpu().numpy(), full.double().cpu().numpy()) < 1e-6
+    a = [torch.full((bounds[t + 1] - bounds[t], n2, n1), 7.0, device="cuda") for t in range(4)]
+    b = [torch.full((bounds[t + 1] - bounds[t], n2, n1), 7.0, device="cuda") for t in range(4)]
+    sc.backproject_cvp_scatter(proj[:5], a, bounds, view_begin=0, view_count=5, store=True)
+    sc.backproject_cvp_scatter(proj[5:], b, bounds, view_begin=5, view_count=len(views) - 5, store=True)
+    out = torch.empty(full.numel(), dtype=torch.float64, device="cuda")
+    sc.sum_slabs([torch.cat(a, 0).reshape(-1), torch.cat(b, 0).reshape(-1)], full.numel(), out)
+    torch.cuda.synchronize()
+    assert rel_l2(out.cpu().numpy(), full.reshape(-1).double().cpu().numpy()) < 1e-6
     sc.close()
 
 
