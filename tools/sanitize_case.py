@@ -39,3 +39,32 @@ bg = grp.backproject_cvp_host(pg)
 grp.close()
 torch.cuda.synchronize()
 print("sanitize case (round 2 paths) ok")
+
+# round 2 (later): relaxed precision on a scene whose bricks take the
+# per-voxel-cut radius (small voxels far from the source), the three-boundary
+# fast walk (voxels ~2-3 rows tall), and the scatter backprojection in store
+# and atomic mode
+det2 = cb.DetectorGeometry.make(64, 48, 0.1, 0.1)
+geom2 = cb.VolumeGeometry.make((16, 16, 64), (0.05, 0.05, 0.05))
+views2 = cb.make_circular_trajectory(700.0, 1100.0, 6, 360.0, det2)
+sc2 = cb.DeviceScene(geom2, det2, views2)
+x2 = torch.rand(geom2.shape(), device="cuda")
+rel = cb.CvpOptions(precision=cb.CvpPrecision.Single)
+p2 = sc2.project_cvp(x2, opts=rel)
+b2 = sc2.backproject_cvp(p2, opts=rel)
+det3 = cb.DetectorGeometry.make(96, 80, 0.1, 0.1)
+geom3 = cb.VolumeGeometry.make((24, 20, 64), (0.15, 0.15, 0.15))
+views3 = cb.make_circular_trajectory(300.0, 500.0, 5, 360.0, det3)
+sc3 = cb.DeviceScene(geom3, det3, views3)
+x3 = torch.rand(geom3.shape(), device="cuda")
+p3 = sc3.project_cvp(x3)
+b3 = sc3.backproject_cvp(p3)
+n1, n2, n3 = geom3.counts
+bounds = [0, 20, 20, n3]
+slabs = [torch.zeros((bounds[t + 1] - bounds[t], n2, n1), device="cuda") for t in range(3)]
+sc3.backproject_cvp_scatter(p3, slabs, bounds, store=True)
+sc3.backproject_cvp_scatter(p3, slabs, bounds)
+out = torch.empty(n1 * n2 * (bounds[1] - bounds[0]), dtype=torch.float64, device="cuda")
+sc3.sum_slabs([slabs[0].reshape(-1), slabs[0].reshape(-1)], out.numel(), out)
+torch.cuda.synchronize()
+print("sanitize case (relaxed radius, three-boundary walk, scatter) ok")
