@@ -242,7 +242,10 @@ struct cvpb_context {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // host path: copy stream + per-chunk events (stack transfers overlap the
     // projector launches of the neighbouring view chunks)
-    static constexpr int kChunks = 4;
+#ifndef CVPB_HOST_CHUNKS
+#define CVPB_HOST_CHUNKS 4
+#endif
+    static constexpr int kChunks = CVPB_HOST_CHUNKS;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_chunk[kChunks] = {};
     cudaEvent_t ev_copy = nullptr;
