@@ -235,7 +235,7 @@ __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene
                                                 int& n0, int& n1, float* depth_min = nullptr,
                                                 float* depth_max = nullptr,
                                                 bool* rows_inside = nullptr, int* r0_out = nullptr,
-                                                int* r1_out = nullptr) {
+                                                int* r1_out = nullptr, float margin_in = -1.f) {
     // corner offsets from the source in float32 (|offset| <~ 1e3 mm: ~6e-5 mm)
     const float xs[2] = {float(sc.minx + i0 * sc.a1 - vc.sx), float(sc.minx + i1 * sc.a1 - vc.sx)};
     const float ys[2] = {float(sc.miny + j0 * sc.a2 - vc.sy), float(sc.miny + j1 * sc.a2 - vc.sy)};
@@ -253,7 +253,8 @@ __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene
     if (depth_min) *depth_min = dmin;
     if (depth_max) *depth_max = dmax;
     if (rows_inside) *rows_inside = false;
-    const float margin = float(0.5 * sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2));
+    // (half the voxel-base diagonal; the kernel passes it precomputed)
+    const float margin = margin_in >= 0.f ? margin_in : float(0.5 * sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2));
     const float dlo = dmin - margin, dhi = dmax + margin;
     if (!(dlo > 0.f) || !(cmin > -1e7f) || !(cmax < 1e7f)) {
         m0 = 1;
@@ -417,6 +418,13 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
     const int rows = sc.rows, cols = sc.cols;
     const size_t npx = size_t(rows) * cols;
     const float h = p.h;
+    // forward: per-scene constants of the footprint thread once per CTA (no
+    // float64 square root / divisions on the per-view G-phase critical path:
+    // P +2% at c3); the backward recomputes them per view (held across the
+    // view loop they cost it 2-8% in register pressure)
+    const float diag_pre = FWD ? float(sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2)) : 0.f;
+    const float b1_over_b2 = FWD ? float(sc.pw / sc.ph) : 0.f;
+    const double inv_a3_pre = FWD ? 1.0 / sc.a3 : 0.0;
     constexpr bool corr = CORR, per_row_r = CCR != 0;
 
     for (int v = vg0; v < vg1; ++v) {
@@ -446,9 +454,9 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             int m0, m1, n0, n1, r0u = 0, r1u = -1;
             bool fixed_ok = true, rows_inside = false;
             float dmin = 0.f, dmax = 0.f;
+            const float diag = FWD ? diag_pre : float(sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2));
             brick_footprint(vc, sc, i0, i1, j0, j1, k0, k1, m0, m1, n0, n1, &dmin, &dmax, &rows_inside,
-                            &r0u, &r1u);
-            const float diag = float(sqrt(sc.a1 * sc.a1 + sc.a2 * sc.a2));
+                            &r0u, &r1u, 0.5f * diag);
             const float fb2 = float(vc.f_over_b2);
             // Row-walk mode of this (brick, view): the fast walk needs every
             // voxel's rows inside the detector (no clamping), a full brick
@@ -470,7 +478,11 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 if (zlo > 0.f || zhi < 0.f) {
                     dz_near = fminf(fabsf(zlo), fabsf(zhi));
                 } else {
-                    const double t = rint(-(sc.minz + (k0 + 0.5) * sc.a3 - vc.s3) / sc.a3);
+                    // (nearest layer to the source plane: a reciprocal
+                    // multiply can only pick a neighbour at a .5 tie, where
+                    // both are half a layer away)
+                    const double zc0 = sc.minz + (k0 + 0.5) * sc.a3 - vc.s3;
+                    const double t = rint(FWD ? -zc0 * inv_a3_pre : -zc0 / sc.a3);
                     dz_near = float(fabs(sc.minz + (k0 + 0.5 + t) * sc.a3 - vc.s3));
                 }
                 float rho2max = 0.f;
@@ -530,11 +542,13 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 // Scale 2^30 / bound keeps every partial inside int32 (float32
                 // evaluation with 5% slack).
                 const float bf = float(vc.b2_over_f);
-                const float b1f = float(vc.b1 / vc.f);
+                const float b1f = float(vc.b2_over_f) * b1_over_b2;  // b1 / f
                 const float area = b1f * dmax * fmaxf(dmax - dmin, 1e-30f * dmax);
                 const float zwin = bf * (dmax + 0.5f * diag);
                 const float bound = s.mu_abs_max * (area * zwin / (dmin * dmin)) * 1.05f;
-                const float q = (bound > 0.f && dmin > 0.f) ? 1073741824.f / bound : 0.f;
+                // (approximate reciprocal: q bound <= 2^30 (1 + 2^-22), far
+                // inside int32 with the bound's 5% slack)
+                const float q = (bound > 0.f && dmin > 0.f) ? 1073741824.f * fast_rcp(bound) : 0.f;
                 // the fixed-point tile needs a finite brick and a normal
                 // float32 scale; otherwise (NaN / Inf voxels, |mu| so small
                 // that 2^30 / bound overflows) every record of this (brick,
