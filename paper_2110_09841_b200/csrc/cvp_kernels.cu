@@ -221,6 +221,17 @@ __device__ __forceinline__ CutRec load_cut(uint32_t sbase, int slot) {
     return r;
 }
 
+// Division on the footprint thread's critical path: the approximate device
+// form (~2 ulp; the footprint needs pixel accuracy, its rigorous bounds
+// carry >= 1e-4 relative slack).
+__host__ __device__ __forceinline__ float fdiv_fp(float a, float b) {
+#ifdef __CUDA_ARCH__
+    return __fdividef(a, b);
+#else
+    return a / b;
+#endif
+}
+
 // Detector rectangle that contains every record a voxel of the brick can
 // emit under view vc: chi1 over the brick's base corners; chi2 over its z
 // range and its depth range widened by half a voxel-base diagonal (bound on
@@ -244,7 +255,7 @@ __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) {
             const float d = w3x * xs[a] + w3y * ys[b];
-            const float c1 = (w1x * xs[a] + w1y * ys[b]) / d;
+            const float c1 = fdiv_fp(w1x * xs[a] + w1y * ys[b], d);
             cmin = fminf(cmin, c1);
             cmax = fmaxf(cmax, c1);
             dmin = fminf(dmin, d);
@@ -265,7 +276,7 @@ __host__ __device__ inline void brick_footprint(const ViewConst& vc, const Scene
     }
     const float fb2 = float(vc.f_over_b2), pp2 = float(vc.pp2);
     const float z0 = float(sc.minz + k0 * sc.a3 - vc.s3), z1 = float(sc.minz + k1 * sc.a3 - vc.s3);
-    const float rlo = 1.f / dlo, rhi = 1.f / dhi;
+    const float rlo = fdiv_fp(1.f, dlo), rhi = fdiv_fp(1.f, dhi);
     // chi2 = pp2 - z fb2 / d is monotone in z and in 1/d: extremes at the corners
     float rmin = INFINITY, rmax = -INFINITY;
     for (float z : {z0, z1})
@@ -494,8 +505,8 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 const bool gate_ok = !corr || dz_near * dz_near > 4e-28f * rho2max;
                 if (k1 == k0 + BK && dl > 0.f && gate_ok) {
                     const float dzm = fmaxf(fabsf(zlo), fabsf(zhi));
-                    const float rdl = 1.f / dl;
-                    const float tr = (0.5f * float(sc.a3) + dzm * ddm / dmin) * fb2 * rdl * 1.0001f + 2e-5f;
+                    const float rdl = fdiv_fp(1.f, dl);
+                    const float tr = (0.5f * float(sc.a3) + fdiv_fp(dzm * ddm, dmin)) * fb2 * rdl * 1.0001f + 2e-5f;
                     mode = 2.f * tr < 0.999f ? 1 : 2.f * tr < 1.999f ? 2 : 2.f * tr < 2.999f ? 3 : 0;
                     // a brick whose rows reach past the detector's top or
                     // bottom edge walks the same rows and drops the records
@@ -545,7 +556,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 const float b1f = float(vc.b2_over_f) * b1_over_b2;  // b1 / f
                 const float area = b1f * dmax * fmaxf(dmax - dmin, 1e-30f * dmax);
                 const float zwin = bf * (dmax + 0.5f * diag);
-                const float bound = s.mu_abs_max * (area * zwin / (dmin * dmin)) * 1.05f;
+                const float bound = s.mu_abs_max * fdiv_fp(area * zwin, dmin * dmin) * 1.05f;
                 // (approximate reciprocal: q bound <= 2^30 (1 + 2^-22), far
                 // inside int32 with the bound's 5% slack)
                 const float q = (bound > 0.f && dmin > 0.f) ? 1073741824.f * fast_rcp(bound) : 0.f;
