@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             const float fb2 = float(vc.f_over_b2);
             // Row-walk mode of this (brick, view): the fast walk needs every
             // voxel's rows inside the detector (no clamping), a full brick
-            // along x3 (no virtual layers) and 2 tr < NB + 1 for every
+            // along x3 (no virtual layers) and 2 tr < NB (<= NB + 1 rows) for every
             // voxel-cut, with the rigorous bound
             //   tr <= h f/(b2 (dmin - dd)) + |dz|max f dd / (b2 dmin (dmin - dd)) + 1e-5,
             // dd = diag/2 >= |hw| halfw (walk_rows_fast, cvp_device.cuh);
