@@ -449,11 +449,39 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             const int tstride = s.tile_stride;
             const float* img = s.img;
             const float* scale = s.scale;
+#ifndef CVP_OLD_PROLOGUE
+            // warps over tile rows, lanes over tile columns (coalesced image
+            // reads, conflict-free column-major stores at the odd stride);
+            // four rows in flight per thread, no integer division
+            const int w0 = t0 >> 5, nw = step >> 5, ln = t0 & 31;
+            for (int c0 = ln; c0 < tcols; c0 += 32) {
+                const float* irow = img + size_t(tm0) * cols + (tn0 + c0);
+                const float* srow = scale + size_t(tm0) * cols + (tn0 + c0);
+                float* tcol = tile + c0 * tstride;
+                int r = w0;
+                for (; r + 3 * nw < trows; r += 4 * nw) {
+                    float a[4], b[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const size_t o = size_t(r + u * nw) * cols;
+                        a[u] = __ldg(irow + o);
+                        b[u] = __ldg(srow + o);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) tcol[r + u * nw] = a[u] * b[u];
+                }
+                for (; r < trows; r += nw) {
+                    const size_t o = size_t(r) * cols;
+                    tcol[r] = __ldg(irow + o) * __ldg(srow + o);
+                }
+            }
+#else
             for (int idx = t0; idx < trows * tcols; idx += step) {
                 const int r = idx / tcols, cc = idx % tcols;
                 const size_t px = size_t(tm0 + r) * cols + (tn0 + cc);
                 tile[cc * tstride + r] = __ldg(img + px) * __ldg(scale + px);
             }
+#endif
         };
         // ---- G-phase: column cuts --------------------------------------
         // Warps past the G-phase columns (NCOL < NT) compute the brick
