@@ -454,25 +454,28 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             // reads, conflict-free column-major stores at the odd stride);
             // four rows in flight per thread, no integer division
             const int w0 = t0 >> 5, nw = step >> 5, ln = t0 & 31;
+            // (virtual rows — tm0 < 0 or past the detector — stage zeros)
             for (int c0 = ln; c0 < tcols; c0 += 32) {
-                const float* irow = img + size_t(tm0) * cols + (tn0 + c0);
-                const float* srow = scale + size_t(tm0) * cols + (tn0 + c0);
+                const float* irow = img + ptrdiff_t(tm0) * cols + (tn0 + c0);
+                const float* srow = scale + ptrdiff_t(tm0) * cols + (tn0 + c0);
                 float* tcol = tile + c0 * tstride;
                 int r = w0;
                 for (; r + 3 * nw < trows; r += 4 * nw) {
                     float a[4], b[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const size_t o = size_t(r + u * nw) * cols;
-                        a[u] = __ldg(irow + o);
-                        b[u] = __ldg(srow + o);
+                        const int rr = r + u * nw;
+                        const bool in = unsigned(tm0 + rr) < unsigned(rows);
+                        const ptrdiff_t o = ptrdiff_t(rr) * cols;
+                        a[u] = in ? __ldg(irow + o) : 0.f;
+                        b[u] = in ? __ldg(srow + o) : 0.f;
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u) tcol[r + u * nw] = a[u] * b[u];
                 }
                 for (; r < trows; r += nw) {
-                    const size_t o = size_t(r) * cols;
-                    tcol[r] = __ldg(irow + o) * __ldg(srow + o);
+                    const ptrdiff_t o = ptrdiff_t(r) * cols;
+                    tcol[r] = unsigned(tm0 + r) < unsigned(rows) ? __ldg(irow + o) * __ldg(srow + o) : 0.f;
                 }
             }
 #else
@@ -542,15 +545,15 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                     // on its own two boundaries, so this is exactly the
                     // reference's clamped range (cvp.cpp:197-201)
                     if (mode && !rows_inside) {
-                        // forward, preferably with virtual rows: the tile
-                        // spans the unclamped row range, records of rows off
-                        // the detector land in tile rows the flush drops, and
-                        // the brick walks the plain fast path (c3 P +1%, c2
-                        // +3%); otherwise (tile too small; the backward, whose
-                        // larger tile staging costs more than the clipping
-                        // saves) the clipping variant of the walk
+                        // preferably with virtual rows: the tile spans the
+                        // unclamped row range, records of rows off the
+                        // detector land in tile rows the forward's flush
+                        // drops and the backward stages as zeros, and the
+                        // brick walks the plain fast path (c3 P +1%, BP +2%;
+                        // c2 P +3%, BP +2-5%); otherwise (tile too small) the
+                        // clipping variant of the walk
                         const int tcu = max(n1 - n0 + 1, 0);
-                        if (FWD && m1 >= m0 && tcu > 0 && ((r1u - r0u + 1) | 1) * tcu <= p.tile_cap) {
+                        if (m1 >= m0 && tcu > 0 && ((r1u - r0u + 1) | 1) * tcu <= p.tile_cap) {
                             m0 = r0u;
                             m1 = r1u;
                         } else {
