@@ -304,10 +304,14 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
 //   T = clamp(alpha, -h, h) + [(s - |alpha+h|)+^2 - (s - |alpha-h|)+^2] / (4s),
 // exact for any s (also ramps wider than the voxel); both squares are <= s^2,
 // so the correction stays bounded as s -> 0 and vanishes at s = 0.
+// spread_of: the spread sh |d| with a 1e-30 floor folded into the multiply
+// (no separate max before the reciprocal; below ulp of any real spread, and
+// with sh = 0 the correction's squares underflow to exactly 0).
+__device__ __forceinline__ float spread_of(float sh, float d) { return fmaf(sh, fabsf(d), 1e-30f); }
 __device__ __forceinline__ float clamp_mean_local(float alpha, float spread, float h) {
     const float d1 = fmaxf(spread - fabsf(alpha + h), 0.f);
     const float d2 = fmaxf(spread - fabsf(alpha - h), 0.f);
-    const float corr = fmaf(d1, d1, -d2 * d2) * (0.25f * fast_rcp(fmaxf(spread, 1e-30f)));
+    const float corr = fmaf(d1, d1, -d2 * d2) * (0.25f * fast_rcp(spread));
     return clampf(alpha, -h, h) + corr;
 }
 
@@ -363,7 +367,7 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
     // included, in all but ~1e-4 of voxel-cuts (the range is built from the
     // voxel's own corners): T = h exactly. The branch is warp-uniform in
     // practice, so the clamp-mean runs only for the rare straddling lane.
-    const float s_top = sh * fabsf(dtop);
+    const float s_top = spread_of(sh, dtop);
     float t_top = h;
     if (a_top - s_top < h) t_top = clamp_mean_local(a_top, s_top, h);
     int m = m_first;
@@ -377,12 +381,12 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
                               make_float2(a_top, a_top));  // alpha at e+1, e+2
         const float p1 = clampf(A.x, -h, h), p2 = clampf(A.y, -h, h);
         const float2 D = add2(make_float2(dtop, dtop), make_float2(-1.f, -2.f));
-        const float s1 = sh * fabsf(D.x), s2 = sh * fabsf(D.y);
+        const float s1 = spread_of(sh, D.x), s2 = spread_of(sh, D.y);
         const float2 AP = add2(A, make_float2(h, h)), AM = sub2(A, make_float2(h, h));
         const float2 d1 = make_float2(fmaxf(s1 - fabsf(AP.x), 0.f), fmaxf(s2 - fabsf(AP.y), 0.f));
         const float2 d2 = make_float2(fmaxf(s1 - fabsf(AM.x), 0.f), fmaxf(s2 - fabsf(AM.y), 0.f));
         const float2 num = sub2(mul2(d1, d1), mul2(d2, d2));
-        const float2 rr = make_float2(fast_rcp(fmaxf(s1, 1e-30f)), fast_rcp(fmaxf(s2, 1e-30f)));
+        const float2 rr = make_float2(fast_rcp(s1), fast_rcp(s2));
         const float2 T = fma2(mul2(num, rr), make_float2(0.25f, 0.25f), make_float2(p1, p2));
         const float t1 = T.x, t2 = T.y;
         const float2 W = sub2(make_float2(t_top, t1), T);
@@ -401,7 +405,7 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
             // third row (boundary e + 3) in straight-line code as well
             const float a3 = fmaf(-3.f, c.g, a_top);
             const float p3 = clampf(a3, -h, h);
-            const float t3 = clamp_mean_local(a3, sh * fabsf(dtop - 3.f), h);
+            const float t3 = clamp_mean_local(a3, spread_of(sh, dtop - 3.f), h);
             float inv3 = inv_r2_fixed;
             if (per_row_r) {
                 const float z3 = fmaf(0.5f, p2 + p3, dz);
@@ -428,7 +432,7 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
         e += 1.f;
         const float a_bot = c.g * (uh - e);
         const float plain_bot = clampf(a_bot, -h, h);
-        const float t_bot = clamp_mean_local(a_bot, sh * fabsf(pmh - e), h);
+        const float t_bot = clamp_mean_local(a_bot, spread_of(sh, pmh - e), h);
         const float share = t_top - t_bot;
         if (DENSE || share > 0.f) {
             float inv_r2 = inv_r2_fixed;
@@ -458,7 +462,11 @@ __device__ __forceinline__ void walk_rows(const CutRec& c, int Mi, float Mf, flo
 // cut's horizontal distance and the voxel's centre height — instead of one
 // per row segment; the launch allows it only where that changes 1/r^2 by
 // <= 2.5e-6 relative (cvp_kernels.cu footprint()).
-template <int NB, class Emit, bool CUTR = false>
+// RAW: rows are emitted biased by +kRowBias (the rounding trick's magic
+// bits left in); the caller folds -kRowBias into its per-cut base address, so
+// no voxel pays the subtraction.
+constexpr int kRowBias = 0x4B400000;
+template <int NB, class Emit, bool CUTR = false, bool RAW = false>
 __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh, float pmh, float dz,
                                                float h, float sh, const bool per_row_r,
                                                float inv_r2_fixed, float wscale, Emit&& emit) {
@@ -470,13 +478,13 @@ __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh
     const float tr = fmaf(fabsf(dz), c.tr_b, c.tr_a);
     // (no +-2^21 guard: the brick's rows lie inside the detector)
     const float clo = __fadd_ru(uh - tr, kMagic - 1.f);
-    const int m_first = Mi + (__float_as_int(clo) - kMagicBits);
+    const int m_first = RAW ? Mi + __float_as_int(clo) : Mi + (__float_as_int(clo) - kMagicBits);
     // first interior boundary (top boundary of row m_first + 1), exact
     const float e1 = clo - (kMagic - 1.f);
     if constexpr (NB == 1) {
         const float a1 = c.g * (uh - e1);
         const float p1 = clampf(a1, -h, h);
-        const float t1 = clamp_mean_local(a1, sh * fabsf(pmh - e1), h);
+        const float t1 = clamp_mean_local(a1, spread_of(sh, pmh - e1), h);
         // weight of a record = max(share, 0) * inv_r2 * wscale
         float2 I = make_float2(inv_r2_fixed * wscale, inv_r2_fixed * wscale);
         if (PRR && per_row_r) {
@@ -499,12 +507,12 @@ __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh
         const float2 A = mul2(make_float2(c.g, c.g), sub2(make_float2(uh, uh), E));
         const float p1 = clampf(A.x, -h, h), p2 = clampf(A.y, -h, h);
         const float2 D = sub2(make_float2(pmh, pmh), E);
-        const float s1 = sh * fabsf(D.x), s2 = sh * fabsf(D.y);
+        const float s1 = spread_of(sh, D.x), s2 = spread_of(sh, D.y);
         const float2 AP = add2(A, make_float2(h, h)), AM = sub2(A, make_float2(h, h));
         const float2 d1 = make_float2(fmaxf(s1 - fabsf(AP.x), 0.f), fmaxf(s2 - fabsf(AP.y), 0.f));
         const float2 d2 = make_float2(fmaxf(s1 - fabsf(AM.x), 0.f), fmaxf(s2 - fabsf(AM.y), 0.f));
         const float2 num = sub2(mul2(d1, d1), mul2(d2, d2));
-        const float2 rr = make_float2(fast_rcp(fmaxf(s1, 1e-30f)), fast_rcp(fmaxf(s2, 1e-30f)));
+        const float2 rr = make_float2(fast_rcp(s1), fast_rcp(s2));
         const float2 T = fma2(mul2(num, rr), make_float2(0.25f, 0.25f), make_float2(p1, p2));
         const float2 S = sub2(make_float2(h, T.x), T);
         if constexpr (NB == 2) {
@@ -527,7 +535,7 @@ __device__ __forceinline__ void walk_rows_fast(const CutRec& c, int Mi, float uh
             const float e3 = e1 + 2.f;
             const float a3 = c.g * (uh - e3);
             const float p3 = clampf(a3, -h, h);
-            const float t3 = clamp_mean_local(a3, sh * fabsf(pmh - e3), h);
+            const float t3 = clamp_mean_local(a3, spread_of(sh, pmh - e3), h);
             const float2 S2 = make_float2(T.y - t3, t3 + h);
             float2 I = make_float2(inv_r2_fixed * wscale, inv_r2_fixed * wscale), I2 = I;
             if (PRR && per_row_r) {

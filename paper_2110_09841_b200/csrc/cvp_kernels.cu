@@ -758,7 +758,9 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 any_active |= v.active;
                 float Mf;  // == float(v.Mi) exactly: not kept (one register per voxel)
                 anchor_at(an, pp2h, float(kk), v.Mi, Mf, v.u0h, v.pmh);
-                v.muq = v.mu * qs;  // forward: fixed-point scale folded into mu
+                // forward: fixed-point scale folded into mu (the rare
+                // off-tile walk re-reads mu itself, so only muq stays live)
+                v.muq = v.mu * qs;
                 v.inv_r2_fixed = per_row_r ? -1.f
                                            : fast_rcp(lds_f32(sbase + uint32_t(offsetof(Smem, rho2c)) + 4u * c) +
                                                       v.dz * v.dz);
@@ -788,7 +790,7 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                     // off the tile (overflow, column outside it): rare, out of line
                     const float ca = offtile_walk<FWD, NR>(
                         r, v.Mi, float(v.Mi), uh, v.pmh, v.dz, h, sh, per_row_r ? 1 : 0, v.inv_r2_fixed,
-                        rows, cols, v.mu, reinterpret_cast<float*>(lds_u64(img_slot)),
+                        rows, cols, FWD ? lds_f32(v.vaddr) : 0.f, reinterpret_cast<float*>(lds_u64(img_slot)),
                         reinterpret_cast<const float*>(lds_u64(scale_slot)),
                         reinterpret_cast<unsigned long long*>(lds_u64(dimg_slot)), lds_f64(detg_slot));
                     if (!FWD) v.acc = fmaf(wA, ca, v.acc);
@@ -817,10 +819,14 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                 constexpr bool CUTR = (MODE & 8) != 0;  // relaxed: one radius per voxel-cut
                 const float sh = corr ? r.shw : 0.f;
                 const float uh = fmaf(v.dz, r.kc, v.u0h);
-                const uint32_t cbase = tbase + 4u * uint32_t((r.n - tn0) * tstride - tm0);
+                // (unclipped: rows arrive biased by kRowBias, folded in here)
+                constexpr bool RAW = !CLIP;
+                const uint32_t cbase =
+                    tbase + 4u * (uint32_t((r.n - tn0) * tstride - tm0) - (RAW ? uint32_t(kRowBias) : 0u));
                 int nrow = 0;
-                auto emit = [&](int m, float w) {
-                    uint32_t a = cbase + 4u * uint32_t(m);
+                auto emit = [&](int m_in, float w) {
+                    uint32_t a = cbase + 4u * uint32_t(m_in);
+                    const int m = RAW ? m_in - kRowBias : m_in;
                     if (CLIP) {
                         // every on-detector row lies in the tile (2-row
                         // margin); the dropped ones write 0 to any tile slot
@@ -837,8 +843,8 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
                         v.acc = fmaf(lds_f32(a), w, v.acc);
                 };
                 const float ws = FWD ? v.muq * r.A : r.A;
-                walk_rows_fast<NB, decltype(emit)&, CUTR>(r, v.Mi, uh, v.pmh, v.dz, h, sh, per_row_r,
-                                                          v.inv_r2_fixed, ws, emit);
+                walk_rows_fast<NB, decltype(emit)&, CUTR, RAW>(r, v.Mi, uh, v.pmh, v.dz, h, sh, per_row_r,
+                                                               v.inv_r2_fixed, ws, emit);
             };
             auto cut = [&](const CutRec& r) {
                 if (tile_ok && unsigned(r.n - tn0) < unsigned(tcols)) {
@@ -860,7 +866,13 @@ __global__ void __launch_bounds__(NT, CVP_MINB) cvp_brick_kernel(CvpParams p) {
             };
             if (any_active) {
                 const int ncached = min(cnt, MAXC);
-                for (int q = 0; q < ncached; ++q) cut(load_cut(sbase, q * NCOL + c));
+                // unrolled over the cut slots (constant record offsets, no
+                // loop counter: c3 P +1-3%, BP +1%)
+#pragma unroll
+                for (int q = 0; q < MAXC; ++q) {
+                    if (q >= ncached) break;
+                    cut(load_cut(sbase, q * NCOL + c));
+                }
                 if (cnt > MAXC) {
                     // overflow (pixels much smaller than voxels): cuts >= MAXC
                     // recomputed out of line, kOverflowCap at a time
